@@ -1,0 +1,84 @@
+// Host-side objects behind the opaque C handles of include/semlab_b200.h.
+#pragma once
+
+#include <array>
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/semlab_b200.h"
+#include "common.hpp"
+#include "kernels.hpp"
+
+struct semlab_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, nranks = 1;
+  void* nccl = nullptr;  // ncclComm_t
+  int64_t launches = 0;
+  sb::DevBuf<double> dot_partial;
+  sb::DevBuf<unsigned> dot_counter;
+  sb::DevBuf<double> dot_out;
+  double* host_pinned = nullptr;  // 64 doubles
+  sb::DotScratch dots() const { return {dot_partial.p, dot_counter.p}; }
+  void count(int64_t n) { launches += n; }
+  // Global sum over ranks of K host doubles (NCCL allreduce on device values when nranks>1).
+  void allreduce_device(double* d_vals, int K);
+  void sync() { SB_CUDA(cudaStreamSynchronize(stream)); }
+  // Deterministic dots of K vector pairs over [off, off+len) summed over ranks; host result.
+  void dots(int K, const double* const* a, const double* const* b, int64_t off, int64_t len, double* host_out);
+};
+
+struct semlab_mesh_s {
+  semlab_ctx ctx = nullptr;
+  std::array<int, 3> dims{};
+  std::function<std::array<double, 3>(double, double, double)> map;
+  double kershaw_eps = 0.0;  // > 0 for generate_kershaw meshes
+  // lattice coordinates of global planes [z0, z0+nz) at an order, (x,y,z) triples x-fastest
+  std::vector<double> lattice_planes(int order, int64_t z0, int64_t nz) const;
+};
+
+struct semlab_space_s {
+  semlab_ctx ctx = nullptr;
+  semlab_mesh mesh = nullptr;
+  int order = 0, bc = SEMLAB_BC_DIRICHLET;
+  sb::Slab sl{};
+  int64_t n = 0, E = 0, nloc = 0;
+  std::vector<double> coords;  // host lattice coords of the local planes (3 per point)
+  sb::DevBuf<double> geom, massw, mass_diag, inv_diag, dep, scratch_e;
+  sb::DevBuf<unsigned> flags, ticket;
+  bool has_inv_diag = false;
+
+  void build();
+  sb::AxSync sync() const { return {dep.p, flags.p, ticket.p}; }
+  // A with an epilogue; handles the slab interface sum when distributed.
+  void apply_A(const double* in, double* out);
+  void ax(const double* in, sb::Epi epi, const sb::EpiArgs& a);
+  const double* jacobi_inv();
+  void stiffness_diag(double* out);
+  int64_t own_off() const { return sl.lidx(0, 0, sl.own_z0()); }
+  int64_t own_len() const { return sl.Nx * sl.Ny * (sl.own_z1() - sl.own_z0()); }
+  double dot(const double* a, const double* b);
+  // Sum partial values on the slab interface planes across ranks (after a Q^T-type op).
+  void interface_sum(double* v);
+};
+
+struct semlab_schwarz_s;
+struct semlab_pmg_s;
+
+struct semlab_op_s {
+  enum Kind { kA, kJacobi, kSchwarz, kPmg, kCallback } kind = kA;
+  semlab_ctx ctx = nullptr;
+  int64_t n = 0;
+  semlab_space space = nullptr;
+  semlab_schwarz_s* sch = nullptr;
+  semlab_pmg_s* pmg = nullptr;
+  semlab_apply_fn fn = nullptr;
+  void* user = nullptr;
+  void apply(const double* in, double* out);
+};
+
+// Thread-local last-error text.
+void sb_set_error(const std::string& msg);

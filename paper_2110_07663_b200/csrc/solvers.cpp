@@ -1,0 +1,352 @@
+// Chebyshev smoother (chebyshev.cpp:58-96), lambda estimate (chebyshev.cpp:9-56), restarted
+// GMRES (krylov.cpp:20-129) and a restated PCG, all over device-resident vectors. The host only
+// keeps the small scalars (Hessenberg, Givens, Chebyshev coefficients) and synchronises once per
+// Krylov iteration.
+#include "solvers.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+#include "host_math.hpp"
+
+using namespace sb;
+
+namespace {
+
+cudaStream_t st(semlab_ctx c) { return c->stream; }
+
+// Fused Chebyshev-Jacobi needs S = diag(A)^-1 of the same space and a single rank (interface
+// planes need the cross-rank sum before the owner epilogue).
+bool fused_jacobi(semlab_op S, semlab_op A) {
+  return S->kind == semlab_op_s::kJacobi && A->kind == semlab_op_s::kA && S->space == A->space &&
+         A->ctx->nranks == 1;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ Chebyshev
+void semlab_cheby_s::init(semlab_op S_, semlab_op A_, const semlab_cheby_params& p) {
+  if (!S_ || !A_) invalid("ChebyshevSmoother: missing operator");
+  if (p.order < 1) invalid("ChebyshevSmoother: order must be >= 1");
+  if (!(p.lambda_min_mult > 0.0) || !(p.lambda_max_mult > p.lambda_min_mult))
+    invalid("ChebyshevSmoother: need 0 < lambda_min_mult < lambda_max_mult");
+  if (!(p.lambda_max_est > 0.0)) invalid("ChebyshevSmoother: lambda_max_est not set");
+  if (S_->n != A_->n) invalid("ChebyshevSmoother: operator sizes differ");
+  S = S_;
+  A = A_;
+  ctx = A_->ctx;
+  params = p;
+  const double lmin = p.lambda_min_mult * p.lambda_max_est;
+  const double lmax = p.lambda_max_mult * p.lambda_max_est;
+  theta = 0.5 * (lmax + lmin);
+  delta = 0.5 * (lmax - lmin);
+  sigma = theta / delta;
+  n = A_->n;
+  r.alloc(size_t(n));
+  t.alloc(size_t(n));
+  sad.alloc(size_t(n));
+  d.alloc(size_t(n));
+}
+
+void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
+  cudaStream_t s = st(ctx);
+  if (fused_jacobi(S, A)) {
+    semlab_space sp = A->space;
+    const double* inv = sp->jacobi_inv();
+    if (x_is_zero) {
+      ctx->count(launch_cheb_jac_zero_init(b, inv, r.p, d.p, theta, n, s));
+    } else {
+      EpiArgs a;
+      a.r = r.p;
+      a.d = d.p;
+      a.b = b;
+      a.inv = inv;
+      a.c1 = theta;
+      sp->ax(x, Epi::ChebJacInit, a);
+    }
+    double rho = 1.0 / sigma;
+    for (int k = 1; k <= params.order; ++k) {
+      const double rho_next = 1.0 / (2.0 * sigma - rho);
+      EpiArgs a;
+      a.x = x;
+      a.r = r.p;
+      a.d = d.p;
+      a.inv = inv;
+      a.c1 = rho_next * rho;
+      a.c2 = 2.0 * rho_next / delta;
+      sp->ax(d.p, Epi::ChebJacStep, a);
+      rho = rho_next;
+    }
+    ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));
+    return;
+  }
+  // generic surrogate S (Schwarz has its own fused path inside the pMG driver)
+  if (x_is_zero) {
+    ctx->count(launch_copy(t.p, b, n, s));
+  } else {
+    A->apply(x, t.p);
+    ctx->count(launch_sub(t.p, b, t.p, n, s));
+  }
+  S->apply(t.p, r.p);
+  ctx->count(launch_cheb_init(r.p, d.p, theta, n, s));
+  double rho = 1.0 / sigma;
+  for (int k = 1; k <= params.order; ++k) {
+    A->apply(d.p, t.p);
+    S->apply(t.p, sad.p);
+    const double rho_next = 1.0 / (2.0 * sigma - rho);
+    ctx->count(launch_cheb_step(x, r.p, d.p, sad.p, rho_next * rho, 2.0 * rho_next / delta, n, s));
+    rho = rho_next;
+  }
+  ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));
+}
+
+namespace sb {
+
+OwnRange own_range_of(semlab_op A) {
+  if (A->space) return {A->space->n, A->space->own_off(), A->space->own_len()};
+  return {A->n, 0, A->n};
+}
+
+namespace {
+
+// Host copies of device reductions (after an allreduce over ranks).
+void fetch(semlab_ctx c, const double* d, double* h, int K) {
+  c->allreduce_device(const_cast<double*>(d), K);
+  SB_CUDA(cudaMemcpyAsync(c->host_pinned, d, sizeof(double) * K, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  for (int k = 0; k < K; ++k) h[k] = c->host_pinned[k];
+}
+
+// One CGS2 Arnoldi step on w against V[:, :ncol] (krylov.cpp:67-76): h (incl. h2), ||w||.
+void cgs2(semlab_ctx c, const OwnRange& o, const double* V, int64_t ldv, int ncol, double* w, double* d_h,
+          std::vector<double>& h, double& hnext) {
+  cudaStream_t s = c->stream;
+  double* d_h2 = d_h + 32;
+  double* d_nrm = d_h + 64;
+  c->count(launch_gemv_t(V, ldv, ncol, w, o.off, o.len, d_h, c->dots(), s));
+  c->allreduce_device(d_h, ncol);
+  c->count(launch_cgs_update_dot(V, ldv, ncol, w, d_h, o.n, o.off, o.len, d_h2, c->dots(), s));
+  c->allreduce_device(d_h2, ncol);
+  c->count(launch_cgs_update_norm(V, ldv, ncol, w, d_h2, o.n, o.off, o.len, d_nrm, c->dots(), s));
+  c->allreduce_device(d_nrm, 1);
+  SB_CUDA(cudaMemcpyAsync(c->host_pinned, d_h, sizeof(double) * 65, cudaMemcpyDeviceToHost, s));
+  c->sync();
+  h.assign(size_t(ncol), 0.0);
+  for (int k = 0; k < ncol; ++k) h[size_t(k)] = c->host_pinned[k] + c->host_pinned[32 + k];
+  hnext = std::sqrt(c->host_pinned[64]);
+}
+
+}  // namespace
+
+semlab_lambda_estimate estimate_lambda_max(semlab_op S, semlab_op A, int64_t n, int rounds, uint64_t seed) {
+  if (rounds < 1) invalid("estimate_lambda_max: rounds >= 1");
+  if (rounds > 31) invalid("estimate_lambda_max: rounds <= 31 on the device path");
+  if (!S || !A || S->n != n || A->n != n) invalid("estimate_lambda_max: operator sizes differ from n");
+  semlab_ctx c = A->ctx;
+  cudaStream_t s = c->stream;
+  const OwnRange o = own_range_of(A);
+  semlab_lambda_estimate est{0.0, 0, 0};
+  // seeded U(-1,1) start vector, one draw per global lattice dof in index order
+  std::vector<double> hv(static_cast<size_t>(n));
+  int64_t offset = 0;
+  if (A->space) offset = A->space->sl.zlo * A->space->sl.Nx * A->space->sl.Ny;
+  uniform_pm1_range(seed, offset, n, hv.data());
+  DevBuf<double> v(static_cast<size_t>(n)), t(static_cast<size_t>(n)), w(static_cast<size_t>(n)), V(size_t(n) * (rounds + 1)), dh(96);
+  v.upload(hv.data(), size_t(n), s);
+  std::vector<double> H(size_t(rounds + 1) * rounds, 0.0);  // column-major (rounds+1) x rounds
+  A->apply(v.p, t.p);
+  S->apply(t.p, w.p);
+  const double* wv[1] = {w.p};
+  double nrm2 = 0.0;
+  c->dots(1, wv, wv, o.off, o.len, &nrm2);
+  const double nrm = std::sqrt(nrm2);
+  if (!(nrm > 0.0)) {
+    est.breakdown = 1;
+    return est;
+  }
+  c->count(launch_div(V.p, w.p, nrm, n, s));
+  int m = 0;
+  std::vector<double> h;
+  for (int j = 0; j < rounds; ++j) {
+    A->apply(V.p + size_t(j) * n, t.p);
+    S->apply(t.p, w.p);
+    double hnext = 0.0;
+    cgs2(c, o, V.p, n, j + 1, w.p, dh.p, h, hnext);
+    for (int i = 0; i <= j; ++i) H[size_t(i) + size_t(rounds + 1) * j] = h[size_t(i)];
+    H[size_t(j + 1) + size_t(rounds + 1) * j] = hnext;
+    m = j + 1;
+    double hmax = 0.0;
+    for (double e : h) hmax = std::max(hmax, std::abs(e));
+    if (hnext <= 1e-12 * hmax) {
+      est.breakdown = 1;
+      break;
+    }
+    c->count(launch_div(V.p + size_t(j + 1) * n, w.p, hnext, n, s));
+  }
+  est.rounds_used = m;
+  std::vector<double> Hm(size_t(m) * m);
+  for (int jj = 0; jj < m; ++jj)
+    for (int i = 0; i < m; ++i) Hm[size_t(i) + size_t(m) * jj] = H[size_t(i) + size_t(rounds + 1) * jj];
+  est.value = max_abs_eig(m, Hm.data());
+  c->sync();
+  return est;
+}
+
+KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, const semlab_gmres_config& cfg) {
+  if (cfg.restart < 1) invalid("gmres: restart must be >= 1");
+  if (cfg.restart > 31) invalid("gmres: restart must be <= 31 on the device path");
+  if (!(cfg.tol > 0.0)) invalid("gmres: tol must be positive");
+  if (!A) invalid("gmres: missing operator");
+  semlab_ctx c = A->ctx;
+  cudaStream_t s = c->stream;
+  const int64_t n = A->n;
+  const int m = cfg.restart;
+  const OwnRange o = own_range_of(A);
+  KrylovResult res;
+  DevBuf<double> r(static_cast<size_t>(n)), w(static_cast<size_t>(n)), z(static_cast<size_t>(n)), V(size_t(n) * (m + 1)), dh(96);
+  auto applyM = [&](const double* in, double* out) {
+    if (M)
+      M->apply(in, out);
+    else
+      c->count(launch_copy(out, in, n, s));
+  };
+  auto norm = [&](const double* v) {
+    const double* av[1] = {v};
+    double r2 = 0.0;
+    c->dots(1, av, av, o.off, o.len, &r2);
+    return std::sqrt(r2);
+  };
+  A->apply(x, r.p);
+  c->count(launch_sub(r.p, b, r.p, n, s));
+  res.initial_residual = norm(r.p);
+  const double target = cfg.use_abs_tol ? cfg.abs_tol : cfg.tol * res.initial_residual;
+  auto finish = [&](double rr) {
+    res.abs_residual = rr;
+    res.rel_residual = res.initial_residual > 0.0 ? rr / res.initial_residual : 0.0;
+  };
+  double beta = res.initial_residual;
+  if (beta <= target) {
+    res.converged = true;
+    finish(beta);
+    return res;
+  }
+  std::vector<double> H(size_t(m + 1) * m, 0.0), g(static_cast<size_t>(m + 1)), cs(static_cast<size_t>(m)), sn(static_cast<size_t>(m)), h;
+  auto Hc = [&](int i, int j) -> double& { return H[size_t(i) + size_t(m + 1) * j]; };
+  while (res.iterations < cfg.max_iters) {
+    c->count(launch_div(V.p, r.p, beta, n, s));
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    bool lucky = false;
+    for (; j < m && res.iterations < cfg.max_iters; ++j) {
+      applyM(V.p + size_t(j) * n, z.p);
+      A->apply(z.p, w.p);
+      double hnext = 0.0;
+      cgs2(c, o, V.p, n, j + 1, w.p, dh.p, h, hnext);
+      for (int i = 0; i <= j; ++i) Hc(i, j) = h[size_t(i)];
+      Hc(j + 1, j) = hnext;
+      for (int i = 0; i < j; ++i) {  // Givens (krylov.cpp:77-89)
+        const double tt = cs[i] * Hc(i, j) + sn[i] * Hc(i + 1, j);
+        Hc(i + 1, j) = -sn[i] * Hc(i, j) + cs[i] * Hc(i + 1, j);
+        Hc(i, j) = tt;
+      }
+      const double denom = std::hypot(Hc(j, j), Hc(j + 1, j));
+      cs[j] = denom > 0.0 ? Hc(j, j) / denom : 1.0;
+      sn[j] = denom > 0.0 ? Hc(j + 1, j) / denom : 0.0;
+      Hc(j, j) = denom;
+      Hc(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] *= cs[j];
+      ++res.iterations;
+      const double res_est = std::abs(g[j + 1]);
+      res.history.push_back(res_est);
+      if (hnext <= 1e-14 * beta) {
+        res.breakdown = true;
+        lucky = true;
+        ++j;
+        break;
+      }
+      c->count(launch_div(V.p + size_t(j + 1) * n, w.p, hnext, n, s));
+      if (res_est <= target) {
+        ++j;
+        break;
+      }
+    }
+    if (j > 0) {  // x += M (V y), krylov.cpp:108-114
+      std::vector<double> y(static_cast<size_t>(j));
+      for (int i = j - 1; i >= 0; --i) {
+        double acc = g[size_t(i)];
+        for (int k = i + 1; k < j; ++k) acc -= Hc(i, k) * y[size_t(k)];
+        y[size_t(i)] = acc / Hc(i, i);
+      }
+      c->count(launch_gemv_n(V.p, n, j, y.data(), w.p, n, s));
+      applyM(w.p, z.p);
+      c->count(launch_axpby(x, 1.0, z.p, 1.0, n, s));
+    }
+    A->apply(x, r.p);
+    c->count(launch_sub(r.p, b, r.p, n, s));
+    beta = norm(r.p);
+    if (beta <= target || lucky) {
+      res.converged = true;
+      finish(beta);
+      return res;
+    }
+  }
+  finish(beta);
+  res.converged = beta <= target;
+  return res;
+}
+
+KrylovResult pcg_solve(semlab_op A, semlab_op M, const double* b, double* x, const semlab_gmres_config& cfg) {
+  if (!(cfg.tol > 0.0)) invalid("pcg: tol must be positive");
+  if (!A) invalid("pcg: missing operator");
+  semlab_ctx c = A->ctx;
+  cudaStream_t s = c->stream;
+  const int64_t n = A->n;
+  const OwnRange o = own_range_of(A);
+  KrylovResult res;
+  DevBuf<double> r(static_cast<size_t>(n)), w(static_cast<size_t>(n)), z(static_cast<size_t>(n)), p(static_cast<size_t>(n));
+  auto dot = [&](const double* a, const double* bb) {
+    const double* av[1] = {a};
+    const double* bv[1] = {bb};
+    double v = 0.0;
+    c->dots(1, av, bv, o.off, o.len, &v);
+    return v;
+  };
+  A->apply(x, w.p);
+  c->count(launch_sub(r.p, b, w.p, n, s));
+  res.initial_residual = std::sqrt(dot(r.p, r.p));
+  const double target = cfg.use_abs_tol ? cfg.abs_tol : cfg.tol * res.initial_residual;
+  double rn = res.initial_residual;
+  if (rn <= target || rn == 0.0) {
+    res.converged = true;
+    res.abs_residual = rn;
+    res.rel_residual = 0.0;
+    return res;
+  }
+  if (M) M->apply(r.p, z.p); else c->count(launch_copy(z.p, r.p, n, s));
+  c->count(launch_copy(p.p, z.p, n, s));
+  double rz = dot(r.p, z.p);
+  while (res.iterations < cfg.max_iters) {
+    A->apply(p.p, w.p);
+    const double alpha = rz / dot(p.p, w.p);
+    c->count(launch_axpby(x, alpha, p.p, 1.0, n, s));
+    c->count(launch_axpby(r.p, -alpha, w.p, 1.0, n, s));
+    ++res.iterations;
+    rn = std::sqrt(dot(r.p, r.p));
+    res.history.push_back(rn);
+    if (rn <= target) break;
+    if (M) M->apply(r.p, z.p); else c->count(launch_copy(z.p, r.p, n, s));
+    const double rz_new = dot(r.p, z.p);
+    c->count(launch_axpby(p.p, 1.0, z.p, rz_new / rz, n, s));
+    rz = rz_new;
+  }
+  A->apply(x, w.p);
+  c->count(launch_sub(w.p, b, w.p, n, s));
+  res.abs_residual = std::sqrt(dot(w.p, w.p));
+  res.rel_residual = res.initial_residual > 0.0 ? res.abs_residual / res.initial_residual : 0.0;
+  res.converged = rn <= target;
+  return res;
+}
+
+}  // namespace sb

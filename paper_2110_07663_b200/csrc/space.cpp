@@ -1,0 +1,183 @@
+// Context, mesh and SemSpace host logic (setup on the host/device, every apply on the device).
+#include <nccl.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "host_math.hpp"
+#include "objects.hpp"
+
+using namespace sb;
+
+#define SB_NCCL(call)                                                                  \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess) fail(kNccl, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// ------------------------------------------------------------------------------ context
+void semlab_ctx_s::allreduce_device(double* d_vals, int K) {
+  if (nranks <= 1) return;
+  SB_NCCL(ncclAllReduce(d_vals, d_vals, size_t(K), ncclDouble, ncclSum, static_cast<ncclComm_t>(nccl), stream));
+}
+
+void semlab_ctx_s::dots(int K, const double* const* a, const double* const* b, int64_t off, int64_t len,
+                        double* host_out) {
+  const double* aa[4];
+  const double* bb[4];
+  for (int k = 0; k < K; ++k) {
+    aa[k] = a[k] + off;
+    bb[k] = b[k] + off;
+  }
+  count(launch_dots(K, aa, bb, len, dot_out.p, dots(), stream));
+  allreduce_device(dot_out.p, K);
+  SB_CUDA(cudaMemcpyAsync(host_pinned, dot_out.p, sizeof(double) * K, cudaMemcpyDeviceToHost, stream));
+  sync();
+  for (int k = 0; k < K; ++k) host_out[k] = host_pinned[k];
+}
+
+// ------------------------------------------------------------------------------ mesh
+// Global GLL-lattice coordinates (mesh.cpp:104-136) for planes [z0, z0+nz) only.
+std::vector<double> semlab_mesh_s::lattice_planes(int order, int64_t z0, int64_t nz) const {
+  const Gll& g = gll(order);
+  std::array<std::vector<double>, 3> axis;
+  for (int d = 0; d < 3; ++d) {
+    const int64_t npts = int64_t(dims[d]) * order + 1;
+    axis[d].resize(size_t(npts));
+    for (int64_t gi = 0; gi < npts; ++gi) {
+      int64_t e = gi / order, i = gi % order;
+      if (e == dims[d]) {
+        e -= 1;
+        i = order;
+      }
+      axis[d][size_t(gi)] = (double(e) + 0.5 * (g.nodes[size_t(i)] + 1.0)) / dims[d];
+    }
+  }
+  const int64_t nx = int64_t(dims[0]) * order + 1, ny = int64_t(dims[1]) * order + 1;
+  std::vector<double> out(size_t(nx * ny * nz) * 3);
+  auto fill = [&](int64_t kk) {
+    const int64_t k = z0 + kk;
+    size_t idx = size_t(kk * nx * ny) * 3;
+    for (int64_t j = 0; j < ny; ++j)
+      for (int64_t i = 0; i < nx; ++i) {
+        const auto p = map(axis[0][size_t(i)], axis[1][size_t(j)], axis[2][size_t(k)]);
+        out[idx++] = p[0];
+        out[idx++] = p[1];
+        out[idx++] = p[2];
+      }
+  };
+  if (kershaw_eps > 0.0) {  // pure C++ map: safe to evaluate in parallel
+#pragma omp parallel for schedule(static)
+    for (int64_t kk = 0; kk < nz; ++kk) fill(kk);
+  } else {
+    for (int64_t kk = 0; kk < nz; ++kk) fill(kk);
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------------------ space
+void semlab_space_s::build() {
+  if (order < 1 || order > 9) invalid("SemSpace: order must be in [1,9] for the device kernels, got " + std::to_string(order));
+  if (ctx->nranks > mesh->dims[2])
+    invalid("SemSpace: more ranks (" + std::to_string(ctx->nranks) + ") than element layers in z (" +
+            std::to_string(mesh->dims[2]) + ")");
+  sl = make_slab(order, mesh->dims[0], mesh->dims[1], mesh->dims[2], ctx->rank, ctx->nranks,
+                 bc == SEMLAB_BC_DIRICHLET);
+  const int nd = order + 1;
+  nloc = int64_t(nd) * nd * nd;
+  E = sl.elems();
+  n = sl.n_local();
+  cudaStream_t s = ctx->stream;
+  coords = mesh->lattice_planes(order, sl.zlo, sl.nzl);
+  DevBuf<double> X(coords.size());
+  X.upload(coords.data(), coords.size(), s);
+  geom.alloc(size_t(E * nloc * 6));
+  massw.alloc(size_t(E * nloc));
+  DevBuf<unsigned long long> bad(1);
+  SB_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), s));
+  ctx->count(launch_geom(sl, X.p, geom.p, massw.p, bad.p, s));
+  unsigned long long hb = 0;
+  SB_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
+  ctx->sync();
+  if (hb != ~0ull) numeric("SemSpace: non-positive Jacobian in element " + std::to_string(hb));
+  mass_diag.alloc(size_t(n));
+  mass_diag.zero(s);
+  ctx->count(launch_gather(sl, massw.p, mass_diag.p, s));
+  interface_sum(mass_diag.p);
+  dep.alloc(size_t(E * nloc));
+  flags.alloc(size_t(std::max<int64_t>(E, 1)));
+  flags.zero(s);
+  ticket.alloc(1);
+  ticket.zero(s);
+  ctx->sync();
+}
+
+void semlab_space_s::interface_sum(double* v) {
+  if (ctx->nranks <= 1) return;
+  invalid("interface_sum: distributed spaces are not enabled in this build");
+}
+
+void semlab_space_s::ax(const double* in, Epi epi, const EpiArgs& a) {
+  ctx->count(launch_ax(sl, in, geom.p, sync(), epi, a, ctx->stream));
+}
+
+void semlab_space_s::apply_A(const double* in, double* out) {
+  if (in == out) invalid("apply_A: in and out must not alias");
+  EpiArgs a;
+  a.w = out;
+  ax(in, Epi::Write, a);
+  interface_sum(out);
+  if (bc == SEMLAB_BC_NEUMANN) {  // r -= mean(r) (sem_space.cpp:207)
+    static thread_local DevBuf<double> ones;
+    if (ones.n < size_t(n)) {
+      ones.alloc(size_t(n));
+      ctx->count(launch_fill(ones.p, n, 1.0, ctx->stream));
+    }
+    const double* av[1] = {out};
+    const double* bv[1] = {ones.p};
+    double sum = 0.0;
+    ctx->dots(1, av, bv, own_off(), own_len(), &sum);
+    const double mean = sum / double(sl.Nx * sl.Ny * sl.Nz);
+    ctx->count(launch_axpby(out, -mean, ones.p, 1.0, n, ctx->stream));
+  }
+}
+
+const double* semlab_space_s::jacobi_inv() {
+  if (!has_inv_diag) {
+    DevBuf<double> d(static_cast<size_t>(n));
+    stiffness_diag(d.p);
+    inv_diag.alloc(size_t(n));
+    ctx->count(launch_invert_masked(sl, d.p, inv_diag.p, ctx->stream));
+    has_inv_diag = true;
+  }
+  return inv_diag.p;
+}
+
+void semlab_space_s::stiffness_diag(double* out) {
+  DevBuf<double> loc(static_cast<size_t>(E * nloc));
+  ctx->count(launch_local_diag(sl, geom.p, loc.p, ctx->stream));
+  ctx->count(launch_fill(out, n, 0.0, ctx->stream));
+  ctx->count(launch_gather(sl, loc.p, out, ctx->stream));
+  interface_sum(out);
+  ctx->count(launch_mask(sl, out, ctx->stream));
+  ctx->sync();  // loc is freed on return
+}
+
+double semlab_space_s::dot(const double* a, const double* b) {
+  const double* av[1] = {a};
+  const double* bv[1] = {b};
+  double r = 0.0;
+  ctx->dots(1, av, bv, own_off(), own_len(), &r);
+  return r;
+}
+
+// ------------------------------------------------------------------------------ operators
+void semlab_op_s::apply(const double* in, double* out) {
+  switch (kind) {
+    case kA: space->apply_A(in, out); break;
+    case kJacobi: ctx->count(launch_mul(out, space->jacobi_inv(), in, n, ctx->stream)); break;
+    case kCallback: fn(user, in, out); break;
+    default: invalid("semlab_op: operator kind not available");
+  }
+}
