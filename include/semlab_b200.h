@@ -91,7 +91,8 @@ typedef struct { /* GmresStats, krylov.hpp:17-25 (history copied into a caller b
 } semlab_gmres_stats;
 
 /* ---- context ------------------------------------------------------------------------------ */
-/* One context per process and GPU. stream == NULL creates a private non-blocking stream. */
+/* One context per process and GPU. All work is ordered on cuda_stream (a cudaStream_t;
+   NULL = the device's default stream, as in the CUDA runtime). */
 int semlab_ctx_create(int device, void* cuda_stream, semlab_ctx* out);
 /* Multi-GPU: rank/nranks over NCCL; nccl_id is the 128-byte ncclUniqueId from rank 0. */
 int semlab_ctx_create_dist(int device, void* cuda_stream, int rank, int nranks,

@@ -46,12 +46,7 @@ static void ctx_init(semlab_ctx c, int device, void* stream) {
   if (device < 0 || device >= ndev) invalid("semlab_ctx_create: no CUDA device " + std::to_string(device));
   SB_CUDA(cudaSetDevice(device));
   c->device = device;
-  if (stream) {
-    c->stream = static_cast<cudaStream_t>(stream);
-  } else {
-    SB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    c->own_stream = true;
-  }
+  c->stream = static_cast<cudaStream_t>(stream);  // NULL = default stream (shared with the caller)
   c->dot_partial.alloc(size_t(kMaxDotBlocks) * 32);
   c->dot_counter.alloc(1);
   c->dot_counter.zero(c->stream);

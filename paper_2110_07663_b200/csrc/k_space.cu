@@ -17,6 +17,7 @@
 //   * the owner applies an epilogue (plain write, residual, or a whole Chebyshev-Jacobi
 //     vector update) so the smoother needs no extra pass over the vectors.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "host_math.hpp"
