@@ -1,0 +1,31 @@
+// Launchers of the Schwarz/FDM kernels (k_fdm.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+
+namespace sb {
+
+// Owner-write epilogue of the RAS kernel. mode 0: out = z. mode 1 (Chebyshev init):
+// r = z, d = z / c1. mode 2 (Chebyshev step): x += d; r -= z; d = c1 d + c2 r.
+struct RasEpi {
+  double* out = nullptr;
+  double* x = nullptr;
+  double* r = nullptr;
+  double* d = nullptr;
+  double c1 = 0.0, c2 = 0.0;
+};
+
+// S: E x 3 x P x P (row-major S(a, a')), L: E x 3 x P eigenvalues (padding: S = 0, L = 1);
+// P = order + 3; precision 32 -> float arrays, 64 -> double arrays.
+int64_t launch_ras(const Slab& sl, int precision, const void* S, const void* L, const double* r, int mode,
+                   const RasEpi& e, cudaStream_t s);
+// ASM: boxes = E x P^3 scratch of the precision's type; out written on the slab's planes.
+int64_t launch_asm(const Slab& sl, int precision, const void* S, const void* L, const double* r, void* boxes,
+                   double* out, cudaStream_t s);
+// fdm_solve on E padded boxes (FP64 in/out).
+int64_t launch_fdm_boxes(int q, int64_t E, int precision, const void* S, const void* L, const double* in,
+                         double* out, cudaStream_t s);
+
+}  // namespace sb

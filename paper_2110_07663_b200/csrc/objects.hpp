@@ -38,6 +38,8 @@ struct semlab_mesh_s {
   double kershaw_eps = 0.0;  // > 0 for generate_kershaw meshes
   // lattice coordinates of global planes [z0, z0+nz) at an order, (x,y,z) triples x-fastest
   std::vector<double> lattice_planes(int order, int64_t z0, int64_t nz) const;
+  // 1-D unit coordinates of the global GLL lattice per axis (mesh.cpp:104-123)
+  std::array<std::vector<double>, 3> lattice_axes(int order) const;
 };
 
 struct semlab_space_s {

@@ -1,0 +1,621 @@
+// p-multigrid: hierarchy setup, transfers, coarse solvers and the V-cycle (Alg. 1).
+#include "pmg.hpp"
+
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+#include "capi_util.hpp"
+#include "host_math.hpp"
+
+using namespace sb;
+
+namespace sb {
+
+double HostCsr::coeff(int64_t i, int64_t j) const {
+  const int* b = idx.data() + ptr[size_t(i)];
+  const int* e = idx.data() + ptr[size_t(i) + 1];
+  const int* it = std::lower_bound(b, e, int(j));
+  return (it != e && *it == int(j)) ? val[size_t(it - idx.data())] : 0.0;
+}
+
+// Element matrices from the reference kernel applied to unit vectors (sem_space.cpp:127-175),
+// assembled like setFromTriplets (duplicates summed in insertion order: ascending element).
+HostCsr assemble_free_matrix(semlab_space sp) {
+  if (sp->bc != SEMLAB_BC_DIRICHLET) invalid("coarse solve: only the Dirichlet problem is supported");
+  if (sp->ctx->nranks > 1) invalid("coarse solve: assemble on a single-rank space");
+  const int q = sp->order, nd = q + 1, nl = nd * nd * nd, nd2 = nd * nd;
+  const int64_t E = sp->E;
+  std::vector<double> geom(size_t(E) * 6 * nl);
+  SB_CUDA(cudaMemcpyAsync(geom.data(), sp->geom.p, geom.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                          sp->ctx->stream));
+  sp->ctx->sync();
+  const Gll& g = gll(q);
+  const double* D = g.diff.data();
+  const Slab& sl = sp->sl;
+  const int64_t fx = sl.Nx - 2, fy = sl.Ny - 2, fz = sl.Nz - 2;
+  const int64_t nfree = fx * fy * fz;
+  std::vector<std::vector<std::pair<int, double>>> rows(static_cast<size_t>(nfree));
+  std::vector<double> in(static_cast<size_t>(nl)), out(static_cast<size_t>(nl)), ur(static_cast<size_t>(nl)), us(static_cast<size_t>(nl)), ut(static_cast<size_t>(nl));
+  std::vector<double> Ae(size_t(nl) * nl);
+  std::vector<int64_t> fidx(static_cast<size_t>(nl));
+  for (int64_t el = 0; el < E; ++el) {
+    const double* G = geom.data() + size_t(el) * 6 * nl;
+    for (int c = 0; c < nl; ++c) {
+      std::fill(in.begin(), in.end(), 0.0);
+      in[size_t(c)] = 1.0;
+      for (int k = 0; k < nd; ++k)
+        for (int j = 0; j < nd; ++j)
+          for (int i = 0; i < nd; ++i) {
+            double dr = 0, ds = 0, dt = 0;
+            for (int m = 0; m < nd; ++m) {
+              dr += D[i + nd * m] * in[size_t(m + nd * j + nd2 * k)];
+              ds += D[j + nd * m] * in[size_t(i + nd * m + nd2 * k)];
+              dt += D[k + nd * m] * in[size_t(i + nd * j + nd2 * m)];
+            }
+            const int idx = i + nd * j + nd2 * k;
+            ur[size_t(idx)] = dr;
+            us[size_t(idx)] = ds;
+            ut[size_t(idx)] = dt;
+          }
+      for (int idx = 0; idx < nl; ++idx) {
+        const double r = ur[size_t(idx)], s = us[size_t(idx)], t = ut[size_t(idx)];
+        const double g0 = G[0 * nl + idx], g1 = G[1 * nl + idx], g2 = G[2 * nl + idx];
+        const double g3 = G[3 * nl + idx], g4 = G[4 * nl + idx], g5 = G[5 * nl + idx];
+        ur[size_t(idx)] = g0 * r + g1 * s + g2 * t;
+        us[size_t(idx)] = g1 * r + g3 * s + g4 * t;
+        ut[size_t(idx)] = g2 * r + g4 * s + g5 * t;
+      }
+      for (int k = 0; k < nd; ++k)
+        for (int j = 0; j < nd; ++j)
+          for (int i = 0; i < nd; ++i) {
+            double acc = 0;
+            for (int m = 0; m < nd; ++m) {
+              acc += D[m + nd * i] * ur[size_t(m + nd * j + nd2 * k)];
+              acc += D[m + nd * j] * us[size_t(i + nd * m + nd2 * k)];
+              acc += D[m + nd * k] * ut[size_t(i + nd * j + nd2 * m)];
+            }
+            Ae[size_t(i + nd * j + nd2 * k) + size_t(nl) * c] = acc;
+          }
+    }
+    const int ex = int(el % sl.Ex), ey = int((el / sl.Ex) % sl.Ey), ez = int(el / (int64_t(sl.Ex) * sl.Ey));
+    for (int k = 0; k < nd; ++k)
+      for (int j = 0; j < nd; ++j)
+        for (int i = 0; i < nd; ++i) {
+          const int64_t x = int64_t(ex) * q + i, y = int64_t(ey) * q + j, z = int64_t(ez) * q + k;
+          fidx[size_t(i + nd * j + nd2 * k)] =
+              sl.masked(x, y, z) ? -1 : (x - 1) + fx * ((y - 1) + fy * (z - 1));
+        }
+    for (int c = 0; c < nl; ++c) {
+      if (fidx[size_t(c)] < 0) continue;
+      for (int r = 0; r < nl; ++r) {
+        if (fidx[size_t(r)] < 0) continue;
+        rows[size_t(fidx[size_t(r)])].push_back({int(fidx[size_t(c)]), Ae[size_t(r) + size_t(nl) * c]});
+      }
+    }
+  }
+  HostCsr A;
+  A.n = A.m = nfree;
+  A.ptr.assign(size_t(nfree) + 1, 0);
+  for (int64_t i = 0; i < nfree; ++i) {
+    auto& row = rows[size_t(i)];
+    std::stable_sort(row.begin(), row.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    int last = -1;
+    for (auto& kv : row) {
+      if (kv.first == last) {
+        A.val.back() += kv.second;
+      } else {
+        A.idx.push_back(kv.first);
+        A.val.push_back(kv.second);
+        last = kv.first;
+      }
+    }
+    A.ptr[size_t(i) + 1] = int64_t(A.idx.size());
+    std::vector<std::pair<int, double>>().swap(row);
+  }
+  return A;
+}
+
+// amg.cpp:12-65
+std::vector<int> amg_aggregate(const HostCsr& A, double theta, int& n_agg) {
+  const int64_t n = A.n;
+  std::vector<std::vector<int>> strong(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    double row_max = 0.0;
+    for (int64_t k = A.ptr[size_t(i)]; k < A.ptr[size_t(i) + 1]; ++k)
+      if (A.idx[size_t(k)] != i) row_max = std::max(row_max, std::abs(A.val[size_t(k)]));
+    if (row_max == 0.0) continue;
+    const double cutoff = theta * row_max;
+    for (int64_t k = A.ptr[size_t(i)]; k < A.ptr[size_t(i) + 1]; ++k) {
+      const int j = A.idx[size_t(k)];
+      if (j != i && std::abs(A.val[size_t(k)]) >= cutoff) strong[size_t(i)].push_back(j);
+    }
+  }
+  std::vector<int> agg(size_t(n), -1);
+  n_agg = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (agg[size_t(i)] >= 0) continue;
+    bool clean = true;
+    for (int j : strong[size_t(i)])
+      if (agg[size_t(j)] >= 0) { clean = false; break; }
+    if (!clean || strong[size_t(i)].empty()) continue;
+    agg[size_t(i)] = n_agg;
+    for (int j : strong[size_t(i)]) agg[size_t(j)] = n_agg;
+    ++n_agg;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (agg[size_t(i)] >= 0) continue;
+    double best = 0.0;
+    int best_agg = -1;
+    for (int j : strong[size_t(i)]) {
+      if (agg[size_t(j)] < 0) continue;
+      const double w = std::abs(A.coeff(i, j));
+      if (w > best) { best = w; best_agg = agg[size_t(j)]; }
+    }
+    if (best_agg >= 0) agg[size_t(i)] = best_agg;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (agg[size_t(i)] < 0) agg[size_t(i)] = n_agg++;
+  return agg;
+}
+
+// Galerkin P^T A P for piecewise-constant P (amg.cpp:100-108): (P^T A)(I, j) = sum_{i in I} a_ij,
+// then sum over j in J, both ascending.
+static HostCsr galerkin(const HostCsr& A, const std::vector<int>& agg, int n_agg) {
+  std::vector<std::vector<int>> members(static_cast<size_t>(n_agg));
+  for (int64_t i = 0; i < A.n; ++i) members[size_t(agg[size_t(i)])].push_back(int(i));
+  HostCsr C;
+  C.n = C.m = n_agg;
+  C.ptr.assign(size_t(n_agg) + 1, 0);
+  std::map<int, double> rowj;
+  std::map<int, double> rowJ;
+  for (int I = 0; I < n_agg; ++I) {
+    rowj.clear();
+    rowJ.clear();
+    for (int i : members[size_t(I)])
+      for (int64_t k = A.ptr[size_t(i)]; k < A.ptr[size_t(i) + 1]; ++k) rowj[A.idx[size_t(k)]] += A.val[size_t(k)];
+    for (auto& kv : rowj) rowJ[agg[size_t(kv.first)]] += kv.second;
+    for (auto& kv : rowJ) {
+      C.idx.push_back(kv.first);
+      C.val.push_back(kv.second);
+    }
+    C.ptr[size_t(I) + 1] = int64_t(C.idx.size());
+  }
+  return C;
+}
+
+std::vector<AmgLevelHost> amg_build(const HostCsr& A0, double theta, int max_levels, int max_coarse_size) {
+  std::vector<AmgLevelHost> levels;
+  HostCsr current = A0;
+  auto invd = [](const HostCsr& A, bool check) {
+    std::vector<double> d(size_t(A.n));
+    for (int64_t i = 0; i < A.n; ++i) {
+      const double a = A.coeff(i, i);
+      if (check && a == 0.0) numeric("AmgHierarchy: zero diagonal at row " + std::to_string(i));
+      d[size_t(i)] = 1.0 / a;
+    }
+    return d;
+  };
+  bool stopped_uncoarsenable = false;
+  while (int(levels.size()) < max_levels - 1 && current.n > max_coarse_size) {
+    AmgLevelHost lvl;
+    lvl.inv_diag = invd(current, true);
+    int n_agg = 0;
+    lvl.agg = amg_aggregate(current, theta, n_agg);
+    lvl.n_agg = n_agg;
+    if (n_agg >= current.n) {  // no coarsening possible: this level is the coarsest
+      lvl.agg.clear();
+      lvl.A = current;
+      levels.push_back(std::move(lvl));
+      stopped_uncoarsenable = true;
+      break;
+    }
+    HostCsr coarse = galerkin(current, lvl.agg, n_agg);
+    lvl.A = std::move(current);
+    levels.push_back(std::move(lvl));
+    current = std::move(coarse);
+  }
+  if (!stopped_uncoarsenable) {
+    AmgLevelHost lvl;
+    lvl.inv_diag = invd(current, false);
+    lvl.A = std::move(current);
+    levels.push_back(std::move(lvl));
+  }
+  return levels;
+}
+
+bool dense_spd_inverse(int64_t n, std::vector<double>& M) {
+  // Cholesky M = L L^T (lower, column-major), then inverse by solving for the identity.
+  std::vector<double> L(M);
+  for (int64_t j = 0; j < n; ++j) {
+    double d = L[size_t(j + n * j)];
+    for (int64_t k = 0; k < j; ++k) d -= L[size_t(j + n * k)] * L[size_t(j + n * k)];
+    if (!(d > 0.0)) return false;
+    d = std::sqrt(d);
+    L[size_t(j + n * j)] = d;
+    for (int64_t i = j + 1; i < n; ++i) {
+      double s = L[size_t(i + n * j)];
+      for (int64_t k = 0; k < j; ++k) s -= L[size_t(i + n * k)] * L[size_t(j + n * k)];
+      L[size_t(i + n * j)] = s / d;
+    }
+  }
+  for (int64_t c = 0; c < n; ++c) {
+    std::vector<double> y(size_t(n), 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int64_t k = 0; k < i; ++k) s -= L[size_t(i + n * k)] * y[size_t(k)];
+      y[size_t(i)] = s / L[size_t(i + n * i)];
+    }
+    for (int64_t i = n - 1; i >= 0; --i) {
+      double s = y[size_t(i)];
+      for (int64_t k = i + 1; k < n; ++k) s -= L[size_t(k + n * i)] * M[size_t(k + n * c)];
+      M[size_t(i + n * c)] = s / L[size_t(i + n * i)];
+    }
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------------ coarse solver
+void CoarseSolver::build(semlab_space space, int m) {
+  sp = space;
+  mode = m;
+  HostCsr A = assemble_free_matrix(sp);
+  nfree = A.n;
+  cudaStream_t s = sp->ctx->stream;
+  rf.alloc(size_t(nfree));
+  zf.alloc(size_t(nfree));
+  if (mode == SEMLAB_COARSE_DIRECT) {
+    if (nfree > 20000)
+      invalid("coarse direct solve is limited to 20000 free dofs (got " + std::to_string(nfree) +
+              "); use SEMLAB_COARSE_AMG");
+    std::vector<double> M(size_t(nfree) * nfree, 0.0), I(size_t(nfree) * nfree, 0.0);
+    for (int64_t i = 0; i < nfree; ++i) {
+      for (int64_t k = A.ptr[size_t(i)]; k < A.ptr[size_t(i) + 1]; ++k) M[size_t(i) + size_t(nfree) * A.idx[size_t(k)]] = A.val[size_t(k)];
+      I[size_t(i) + size_t(nfree) * i] = 1.0;
+    }
+    DevBuf<double> dM(M.size());
+    Minv.alloc(I.size());
+    dM.upload(M.data(), M.size(), s);
+    Minv.upload(I.data(), I.size(), s);
+    cusolverDnHandle_t h;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(kCuda, "cusolverDnCreate failed");
+    cusolverDnSetStream(h, s);
+    int lwork = 0;
+    cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, int(nfree), dM.p, int(nfree), &lwork);
+    DevBuf<double> work(size_t(std::max(lwork, 1)));
+    DevBuf<int> info(1);
+    cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, int(nfree), dM.p, int(nfree), work.p, lwork, info.p);
+    cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, int(nfree), int(nfree), dM.p, int(nfree), Minv.p, int(nfree), info.p);
+    int hinfo = 0;
+    SB_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    sp->ctx->sync();
+    cusolverDnDestroy(h);
+    if (hinfo != 0) numeric("coarse solve: factorization failed (info " + std::to_string(hinfo) + ")");
+    return;
+  }
+  // AMG (amg.cpp:69-129): host setup, device V-cycle
+  auto hl = amg_build(A);
+  lev.resize(hl.size());
+  for (size_t l = 0; l < hl.size(); ++l) {
+    Lev& L = lev[l];
+    const AmgLevelHost& H = hl[l];
+    L.n = H.A.n;
+    L.ptr.alloc(H.A.ptr.size());
+    L.ptr.upload(H.A.ptr.data(), H.A.ptr.size(), s);
+    L.idx.alloc(std::max<size_t>(H.A.idx.size(), 1));
+    if (!H.A.idx.empty()) L.idx.upload(H.A.idx.data(), H.A.idx.size(), s);
+    L.val.alloc(std::max<size_t>(H.A.val.size(), 1));
+    if (!H.A.val.empty()) L.val.upload(H.A.val.data(), H.A.val.size(), s);
+    L.inv_diag.alloc(size_t(L.n));
+    L.inv_diag.upload(H.inv_diag.data(), size_t(L.n), s);
+    L.r.alloc(size_t(L.n));
+    L.z.alloc(size_t(L.n));
+    L.t.alloc(size_t(L.n));
+    if (!H.agg.empty()) {
+      L.nc = H.n_agg;
+      L.agg.alloc(H.agg.size());
+      L.agg.upload(H.agg.data(), H.agg.size(), s);
+      std::vector<int64_t> aptr(size_t(H.n_agg) + 1, 0);
+      for (int a : H.agg) aptr[size_t(a) + 1]++;
+      for (int I = 0; I < H.n_agg; ++I) aptr[size_t(I) + 1] += aptr[size_t(I)];
+      std::vector<int> amem(H.agg.size());
+      std::vector<int64_t> fillp(aptr.begin(), aptr.end() - 1);
+      for (int64_t i = 0; i < L.n; ++i) amem[size_t(fillp[size_t(H.agg[size_t(i)])]++)] = int(i);
+      L.aptr.alloc(aptr.size());
+      L.aptr.upload(aptr.data(), aptr.size(), s);
+      L.amem.alloc(amem.size());
+      L.amem.upload(amem.data(), amem.size(), s);
+    }
+  }
+  const HostCsr& Ac = hl.back().A;
+  coarse_n = Ac.n;
+  std::vector<double> M(size_t(coarse_n) * coarse_n, 0.0);
+  for (int64_t i = 0; i < coarse_n; ++i)
+    for (int64_t k = Ac.ptr[size_t(i)]; k < Ac.ptr[size_t(i) + 1]; ++k)
+      M[size_t(i) + size_t(coarse_n) * Ac.idx[size_t(k)]] = Ac.val[size_t(k)];
+  if (!dense_spd_inverse(coarse_n, M)) numeric("AmgHierarchy: coarse factorization failed");
+  coarse_inv.alloc(M.size());
+  coarse_inv.upload(M.data(), M.size(), s);
+  sp->ctx->sync();
+}
+
+// AmgHierarchy::cycle (amg.cpp:140-160) with pre = post = 1 damped-Jacobi sweeps.
+void CoarseSolver::amg_cycle(int l, const double* r, double* z) {
+  semlab_ctx c = sp->ctx;
+  cudaStream_t s = c->stream;
+  Lev& L = lev[size_t(l)];
+  if (l == int(lev.size()) - 1) {
+    c->count(launch_symv(coarse_inv.p, coarse_n, r, z, s));
+    return;
+  }
+  const CsrDev A{L.n, L.ptr.p, L.idx.p, L.val.p};
+  c->count(launch_amg_jacobi0(L.inv_diag.p, omega, r, z, L.n, s));
+  Lev& N = lev[size_t(l) + 1];
+  c->count(launch_amg_restrict(A, L.aptr.p, L.amem.p, L.nc, r, z, N.r.p, s));
+  amg_cycle(l + 1, N.r.p, N.z.p);
+  c->count(launch_amg_prolong(L.agg.p, N.z.p, z, L.n, s));
+  c->count(launch_amg_relax(A, L.inv_diag.p, omega, r, z, L.t.p, s));
+  c->count(launch_copy(z, L.t.p, L.n, s));
+}
+
+void CoarseSolver::solve(const double* r_full, double* z_full) {
+  semlab_ctx c = sp->ctx;
+  cudaStream_t s = c->stream;
+  c->count(launch_gather_free(sp->sl, r_full, rf.p, s));
+  if (mode == SEMLAB_COARSE_DIRECT)
+    c->count(launch_symv(Minv.p, nfree, rf.p, zf.p, s));
+  else
+    amg_cycle(0, rf.p, zf.p);
+  c->count(launch_scatter_free(sp->sl, zf.p, z_full, s));
+}
+
+}  // namespace sb
+
+// ------------------------------------------------------------------------ hierarchy
+static Grid3 grid_of(const Slab& sl) {
+  Grid3 g;
+  g.N[0] = sl.Nx;
+  g.N[1] = sl.Ny;
+  g.N[2] = sl.Nz;
+  g.nxl = sl.Nx;
+  g.nyl = sl.Ny;
+  g.zoff = sl.zlo;
+  g.dirichlet = sl.dirichlet;
+  return g;
+}
+
+semlab_pmg_s::~semlab_pmg_s() {
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  for (auto& L : lv) {
+    delete L.cheb;
+    delete L.A;
+    delete L.S;
+    delete L.sch;
+    delete L.sp;
+  }
+}
+
+void semlab_pmg_s::build() {
+  const size_t nl = orders.size();
+  if (nl < 2) invalid("pmg: schedule needs at least two levels");
+  for (size_t l = 0; l + 1 < nl; ++l)
+    if (!(orders[l] > orders[l + 1])) invalid("pmg: schedule must be strictly decreasing");
+  if (orders.back() != 1) invalid("pmg: schedule must end at order 1");
+  if (ctx->nranks > 1) invalid("pmg: distributed hierarchies are not enabled in this build");
+  lv.resize(nl);
+  for (size_t l = 0; l < nl; ++l) {
+    Level& L = lv[l];
+    auto sp = std::make_unique<semlab_space_s>();
+    sp->ctx = ctx;
+    sp->mesh = mesh;
+    sp->order = orders[l];
+    sp->bc = SEMLAB_BC_DIRICHLET;
+    sp->build();
+    L.sp = sp.release();
+    const int64_t n = L.sp->n;
+    L.b.alloc(size_t(n));
+    L.x.alloc(size_t(n));
+    L.r.alloc(size_t(n));
+    L.b.zero(ctx->stream);
+    L.x.zero(ctx->stream);
+    L.r.zero(ctx->stream);
+    if (l + 1 == nl) break;
+    L.A = new semlab_op_s;
+    L.A->kind = semlab_op_s::kA;
+    L.A->ctx = ctx;
+    L.A->n = n;
+    L.A->space = L.sp;
+    L.S = new semlab_op_s;
+    L.S->ctx = ctx;
+    L.S->n = n;
+    L.S->space = L.sp;
+    if (smoother == SEMLAB_SMOOTHER_JACOBI) {
+      L.S->kind = semlab_op_s::kJacobi;
+      L.sp->jacobi_inv();
+    } else {
+      auto sch = std::make_unique<semlab_schwarz_s>();
+      sch->space = L.sp;
+      sch->mode = smoother == SEMLAB_SMOOTHER_RAS ? SEMLAB_SCHWARZ_RAS : SEMLAB_SCHWARZ_ASM;
+      sch->precision = precision;
+      sch->build();
+      L.sch = sch.release();
+      L.S->kind = semlab_op_s::kSchwarz;
+      L.S->sch = L.sch;
+    }
+    L.lam = estimate_lambda_max(L.S, L.A, n, 10, 0).value;
+    if (!(L.lam > 0.0)) numeric("pmg: lambda estimate failed on level " + std::to_string(l));
+    semlab_cheby_params p{cheb_order, lmin, lmax, L.lam};
+    L.cheb = new semlab_cheby_s;
+    L.cheb->init(L.S, L.A, p);
+  }
+  J.resize(nl - 1);
+  size_t scratch = 0;
+  for (size_t l = 0; l + 1 < nl; ++l) {
+    const int qf = orders[l], qc = orders[l + 1];
+    const auto Jv = lagrange_interpolation_matrix(gll(qc).nodes, gll(qf).nodes);
+    std::memset(&J[l], 0, sizeof(Jmat));
+    for (size_t t = 0; t < Jv.size(); ++t) J[l].v[t] = Jv[t];
+    const Slab& f = lv[l].sp->sl;
+    const Slab& c = lv[l + 1].sp->sl;
+    scratch = std::max<size_t>(scratch, size_t(c.Nx * f.Ny * f.nzl));
+  }
+  tA.alloc(scratch);
+  tB.alloc(scratch);
+  coarse.build(lv.back().sp, coarse_mode);
+  ctx->sync();
+}
+
+// P: coarse level l+1 -> fine level l (three 1-D passes: z, y, x)
+void semlab_pmg_s::prolong(int l, const double* cv, double* fv) {
+  const Slab& f = lv[size_t(l)].sp->sl;
+  const Slab& c = lv[size_t(l) + 1].sp->sl;
+  const int qf = f.q, qc = c.q;
+  cudaStream_t s = ctx->stream;
+  Grid3 gc = grid_of(c), gf = grid_of(f);
+  Grid3 g1 = gc;  // (Ncx, Ncy, fine z)
+  g1.N[2] = f.Nz;
+  g1.zoff = f.zlo;
+  Grid3 g2 = g1;  // (Ncx, Nfy, fine z)
+  g2.N[1] = f.Ny;
+  g2.nyl = f.Ny;
+  const int64_t zb = int64_t(f.ez0) * qf, nz = int64_t(f.ez1 - f.ez0) * qf + 1;
+  ctx->count(launch_transfer_pass(true, cv, gc, tA.p, g1, 2, J[size_t(l)], qf, qc, f.Ez, true, gc, false, gf, zb, nz, s));
+  ctx->count(launch_transfer_pass(true, tA.p, g1, tB.p, g2, 1, J[size_t(l)], qf, qc, f.Ey, false, gc, false, gf, zb, nz, s));
+  ctx->count(launch_transfer_pass(true, tB.p, g2, fv, gf, 0, J[size_t(l)], qf, qc, f.Ex, false, gc, true, gf, zb, nz, s));
+}
+
+// P^T: fine level l -> coarse level l+1 (passes x, y, z)
+void semlab_pmg_s::restrict_(int l, const double* fv, double* cv) {
+  const Slab& f = lv[size_t(l)].sp->sl;
+  const Slab& c = lv[size_t(l) + 1].sp->sl;
+  const int qf = f.q, qc = c.q;
+  cudaStream_t s = ctx->stream;
+  Grid3 gc = grid_of(c), gf = grid_of(f);
+  Grid3 g1 = gf;  // (Ncx, Nfy, fine z)
+  g1.N[0] = c.Nx;
+  g1.nxl = c.Nx;
+  Grid3 g2 = g1;  // (Ncx, Ncy, fine z)
+  g2.N[1] = c.Ny;
+  g2.nyl = c.Ny;
+  const int64_t zbf = int64_t(f.ez0) * qf, nzf = int64_t(f.ez1 - f.ez0) * qf + 1;
+  const int64_t zbc = int64_t(c.ez0) * qc, nzc = int64_t(c.ez1 - c.ez0) * qc + 1;
+  ctx->count(launch_transfer_pass(false, fv, gf, tA.p, g1, 0, J[size_t(l)], qf, qc, f.Ex, true, gf, false, gc, zbf, nzf, s));
+  ctx->count(launch_transfer_pass(false, tA.p, g1, tB.p, g2, 1, J[size_t(l)], qf, qc, f.Ey, false, gf, false, gc, zbf, nzf, s));
+  ctx->count(launch_transfer_pass(false, tB.p, g2, cv, gc, 2, J[size_t(l)], qf, qc, f.Ez, false, gf, true, gc, zbc, nzc, s));
+}
+
+// Alg. 1 with x0 = 0: pre-smooth, residual, restrict, recurse, correct, post-smooth.
+void semlab_pmg_s::cycle(int l) {
+  Level& L = lv[size_t(l)];
+  cudaStream_t s = ctx->stream;
+  if (l == int(lv.size()) - 1) {
+    coarse.solve(L.b.p, L.x.p);
+    return;
+  }
+  const int64_t n = L.sp->n;
+  SB_CUDA(cudaMemsetAsync(L.x.p, 0, size_t(n) * sizeof(double), s));
+  L.cheb->smooth(L.b.p, L.x.p, true);
+  EpiArgs a;
+  a.w = L.r.p;
+  a.b = L.b.p;
+  L.sp->ax(L.x.p, Epi::Residual, a);
+  restrict_(l, L.r.p, lv[size_t(l) + 1].b.p);
+  cycle(l + 1);
+  prolong(l, lv[size_t(l) + 1].x.p, L.r.p);
+  ctx->count(launch_axpby(L.x.p, 1.0, L.r.p, 1.0, n, s));
+  L.cheb->smooth(L.b.p, L.x.p, false);
+}
+
+void semlab_pmg_s::vcycle(const double* b, double* z) {
+  const int64_t n = lv[0].sp->n;
+  ctx->count(launch_copy(lv[0].b.p, b, n, ctx->stream));
+  cycle(0);
+  ctx->count(launch_copy(z, lv[0].x.p, n, ctx->stream));
+}
+
+extern "C" {
+
+int semlab_pmg_create(semlab_mesh mesh, int nlevels, const int* orders, int smoother, int cheb_order, double lmin,
+                      double lmax, int precision, int coarse, semlab_pmg* out) {
+  return guard([&] {
+    need(mesh, "pmg: mesh");
+    need(orders, "pmg: orders");
+    need(out, "pmg: out");
+    if (smoother < 0 || smoother > 2) invalid("pmg: unknown smoother");
+    if (coarse != SEMLAB_COARSE_DIRECT && coarse != SEMLAB_COARSE_AMG) invalid("pmg: unknown coarse solver");
+    if (precision != 32 && precision != 64) invalid("pmg: precision must be 32 or 64");
+    auto p = std::make_unique<semlab_pmg_s>();
+    p->ctx = mesh->ctx;
+    p->mesh = mesh;
+    p->orders.assign(orders, orders + nlevels);
+    p->smoother = smoother;
+    p->cheb_order = cheb_order;
+    p->lmin = lmin;
+    p->lmax = lmax;
+    p->precision = precision;
+    p->coarse_mode = coarse;
+    p->build();
+    *out = p.release();
+  });
+}
+
+int semlab_pmg_destroy(semlab_pmg p) {
+  return guard([&] { delete p; });
+}
+
+int semlab_pmg_vcycle(semlab_pmg p, const double* b, double* z) {
+  return guard([&] {
+    need(p, "pmg: hierarchy");
+    p->vcycle(b, z);
+  });
+}
+
+int semlab_pmg_space(semlab_pmg p, int level, semlab_space* out) {
+  return guard([&] {
+    need(p, "pmg: hierarchy");
+    if (level < 0 || level >= int(p->lv.size())) invalid("pmg: level out of range");
+    *out = p->lv[size_t(level)].sp;
+  });
+}
+
+int semlab_pmg_lambda(semlab_pmg p, int level, double* out) {
+  return guard([&] {
+    need(p, "pmg: hierarchy");
+    if (level < 0 || level + 1 >= int(p->lv.size())) invalid("pmg: level has no smoother");
+    *out = p->lv[size_t(level)].lam;
+  });
+}
+
+int semlab_pmg_prolong(semlab_pmg p, int level, const double* c, double* f) {
+  return guard([&] {
+    need(p, "pmg: hierarchy");
+    if (level < 0 || level + 1 >= int(p->lv.size())) invalid("pmg: level out of range");
+    p->prolong(level, c, f);
+  });
+}
+
+int semlab_pmg_restrict(semlab_pmg p, int level, const double* f, double* c) {
+  return guard([&] {
+    need(p, "pmg: hierarchy");
+    if (level < 0 || level + 1 >= int(p->lv.size())) invalid("pmg: level out of range");
+    p->restrict_(level, f, c);
+  });
+}
+
+int semlab_op_pmg(semlab_pmg p, semlab_op* out) {
+  return guard([&] {
+    need(p, "semlab_op_pmg: hierarchy");
+    auto o = std::make_unique<semlab_op_s>();
+    o->kind = semlab_op_s::kPmg;
+    o->ctx = p->ctx;
+    o->n = p->lv[0].sp->n;
+    o->space = p->lv[0].sp;
+    o->pmg = p;
+    *out = o.release();
+  });
+}
+
+}  // extern "C"

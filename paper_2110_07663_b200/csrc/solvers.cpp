@@ -8,6 +8,7 @@
 #include <cmath>
 
 #include "host_math.hpp"
+#include "schwarz.hpp"
 
 using namespace sb;
 
@@ -20,6 +21,11 @@ cudaStream_t st(semlab_ctx c) { return c->stream; }
 bool fused_jacobi(semlab_op S, semlab_op A) {
   return S->kind == semlab_op_s::kJacobi && A->kind == semlab_op_s::kA && S->space == A->space &&
          A->ctx->nranks == 1;
+}
+
+bool fused_ras(semlab_op S, semlab_op A) {
+  return S->kind == semlab_op_s::kSchwarz && S->sch->mode == SEMLAB_SCHWARZ_RAS && A->kind == semlab_op_s::kA &&
+         S->space == A->space && A->ctx->nranks == 1;
 }
 
 }  // namespace
@@ -46,6 +52,11 @@ void semlab_cheby_s::init(semlab_op S_, semlab_op A_, const semlab_cheby_params&
   t.alloc(size_t(n));
   sad.alloc(size_t(n));
   d.alloc(size_t(n));
+  // the fused RAS path writes only owned (free) nodes: masked entries must stay exactly 0
+  r.zero(ctx->stream);
+  t.zero(ctx->stream);
+  sad.zero(ctx->stream);
+  d.zero(ctx->stream);
 }
 
 void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
@@ -80,7 +91,43 @@ void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
     ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));
     return;
   }
-  // generic surrogate S (Schwarz has its own fused path inside the pMG driver)
+  if (fused_ras(S, A)) {
+    // S = RAS: t = A d in the fused Ax kernel, then the RAS owner write carries the whole
+    // Chebyshev update (x += d; r -= S t; d = c1 d + c2 r).
+    semlab_space sp = A->space;
+    semlab_schwarz_s* sch = S->sch;
+    RasEpi e;
+    e.r = r.p;
+    e.d = d.p;
+    e.c1 = theta;
+    if (x_is_zero) {
+      sch->ras(b, 1, e);  // r = S (b - A 0) = S b
+    } else {
+      EpiArgs a;
+      a.w = t.p;
+      a.b = b;
+      sp->ax(x, Epi::Residual, a);
+      sch->ras(t.p, 1, e);
+    }
+    double rho = 1.0 / sigma;
+    for (int k = 1; k <= params.order; ++k) {
+      const double rho_next = 1.0 / (2.0 * sigma - rho);
+      EpiArgs a;
+      a.w = t.p;
+      sp->ax(d.p, Epi::Write, a);
+      RasEpi es;
+      es.x = x;
+      es.r = r.p;
+      es.d = d.p;
+      es.c1 = rho_next * rho;
+      es.c2 = 2.0 * rho_next / delta;
+      sch->ras(t.p, 2, es);
+      rho = rho_next;
+    }
+    ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));
+    return;
+  }
+  // generic surrogate S
   if (x_is_zero) {
     ctx->count(launch_copy(t.p, b, n, s));
   } else {

@@ -7,6 +7,8 @@
 
 #include "host_math.hpp"
 #include "objects.hpp"
+#include "pmg.hpp"
+#include "schwarz.hpp"
 
 using namespace sb;
 
@@ -39,7 +41,7 @@ void semlab_ctx_s::dots(int K, const double* const* a, const double* const* b, i
 
 // ------------------------------------------------------------------------------ mesh
 // Global GLL-lattice coordinates (mesh.cpp:104-136) for planes [z0, z0+nz) only.
-std::vector<double> semlab_mesh_s::lattice_planes(int order, int64_t z0, int64_t nz) const {
+std::array<std::vector<double>, 3> semlab_mesh_s::lattice_axes(int order) const {
   const Gll& g = gll(order);
   std::array<std::vector<double>, 3> axis;
   for (int d = 0; d < 3; ++d) {
@@ -54,6 +56,11 @@ std::vector<double> semlab_mesh_s::lattice_planes(int order, int64_t z0, int64_t
       axis[d][size_t(gi)] = (double(e) + 0.5 * (g.nodes[size_t(i)] + 1.0)) / dims[d];
     }
   }
+  return axis;
+}
+
+std::vector<double> semlab_mesh_s::lattice_planes(int order, int64_t z0, int64_t nz) const {
+  const auto axis = lattice_axes(order);
   const int64_t nx = int64_t(dims[0]) * order + 1, ny = int64_t(dims[1]) * order + 1;
   std::vector<double> out(size_t(nx * ny * nz) * 3);
   auto fill = [&](int64_t kk) {
@@ -177,6 +184,8 @@ void semlab_op_s::apply(const double* in, double* out) {
   switch (kind) {
     case kA: space->apply_A(in, out); break;
     case kJacobi: ctx->count(launch_mul(out, space->jacobi_inv(), in, n, ctx->stream)); break;
+    case kSchwarz: sch->apply(in, out); break;
+    case kPmg: pmg->vcycle(in, out); break;
     case kCallback: fn(user, in, out); break;
     default: invalid("semlab_op: operator kind not available");
   }
