@@ -1,0 +1,323 @@
+"""Benchmark of the SE pressure-Poisson solve (BASELINE.json metric) — one JSON line on rank 0.
+
+Workload (configs[3], the config the 1/2/4/8-GPU metric is quoted on): Kershaw-deformed box
+eps=0.3, E=32^3, p=7, GMRES(20) to 1e-8 preconditioned by a Chebyshev(2)-RAS p-multigrid V-cycle
+(7,3,1) with FP32 FDM smoother, FP64 Krylov and one AMG V-cycle as the p=1 coarse solve.
+A step = one full solve from x0 = 0 (time-to-1e-8). value = n * iterations / t (GDOF*iter/s).
+
+  python bench.py [--gpus N --steps K --warmup W]        # our sm_100a path (torchrun for N>1)
+  python bench.py --impl reference ...                    # the reference's CPU path on host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Poisson solve GDOF*iter/s (time-to-1e-8)"
+UNIT = "GDOF*iter/s"
+CONFIGS = {
+    "c4": dict(eps=0.3, E=32, p=7, orders=(7, 3, 1), smoother="ras", eta=2, precision=32, coarse="amg",
+               krylov="gmres"),
+    "c2": dict(eps=1.0, E=16, p=7, orders=(7, 3, 1), smoother="jacobi", eta=2, precision=64, coarse="direct",
+               krylov="pcg"),
+    "c3": dict(eps=1.0, E=16, p=7, orders=(7, 3, 1), smoother="ras", eta=2, precision=32, coarse="direct",
+               krylov="gmres"),
+    "c5": dict(eps=0.3, E=96, p=7, orders=(7, 3, 1), smoother="ras", eta=2, precision=32, coarse="amg",
+               krylov="gmres"),
+}
+
+
+def describe(name, c):
+    return (f"{name}: Kershaw eps={c['eps']} E={c['E']}^3 p={c['p']}, {c['krylov'].upper()}"
+            f"{'(20)' if c['krylov'] == 'gmres' else ''} tol 1e-8, Cheby({c['eta']})-{c['smoother'].upper()} "
+            f"pMG{c['orders']} FP{c['precision']} smoother, coarse {c['coarse']}")
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 6 for i in range(4) if r[2 + i] == "Active"})
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------- CPU baselines
+def cpu_reference_sample(cfg, seconds=15.0):
+    """The reference's CPU path on host cores: oracle/_ref (the reference's own sources compiled
+    against the Eigen-API shim, single-threaded like the reference) when it was built, else the
+    numpy port. Bounded sample: the same solver configuration on an E=8^3 mesh, GMRES iterations
+    timed until ~`seconds` of CPU work; GDOF*iter/s is per-dof normalised."""
+    ref = os.path.join(ROOT, "oracle", "_ref", "semlab_ref_bench")
+    E = 8
+    if os.path.exists(ref):
+        out = subprocess.run([ref, "--eps", str(cfg["eps"]), "--elems", str(E), "--order", str(cfg["p"]),
+                              "--smoother", cfg["smoother"], "--coarse", cfg["coarse"], "--cheb-order",
+                              str(cfg["eta"]), "--krylov", cfg["krylov"], "--seconds", str(seconds)],
+                             capture_output=True, text=True, check=True).stdout
+        r = json.loads(out.strip().splitlines()[-1])
+        return {"value": r["gdof_iter_per_s"], "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"reference semlab (shim-compiled) + restated pMG/PCG, eps={cfg['eps']} E={E}^3 "
+                          f"p={cfg['p']}, {r['iters']} iterations in {r['t_solve_s']:.1f}s"}
+    import numpy as np
+    from oracle import semlab_np as o
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    mesh = o.generate_kershaw(cfg["eps"], E)
+    pmg = o.Pmg(mesh, cfg["orders"], cfg["smoother"], cfg["eta"], 0.1, 1.1, cfg["coarse"], cfg["precision"])
+    sp = pmg.spaces[0]
+    b = o.build_rhs(sp, 1)
+    iters, t = 0, 0.0
+    while t < seconds and iters < 200:
+        x = np.zeros(sp.n)
+        t0 = time.perf_counter()
+        st = o.gmres_solve(sp.apply_A, pmg.vcycle, b, x, o.GmresConfig(restart=20, tol=1e-8, max_iters=5))
+        t += time.perf_counter() - t0
+        iters += st.iterations
+    return {"value": sp.n * iters / t / 1e9, "unit": UNIT, "cores": int(os.environ.get("OMP_NUM_THREADS", "1")),
+            "kind": "port", "sample": f"numpy oracle port, eps={cfg['eps']} E={E}^3 p={cfg['p']}, "
+                                      f"{iters} GMRES iterations in {t:.1f}s"}
+
+
+def run_reference(args, cfg, name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per_step = []
+    cb = None
+    for k in range(args.warmup + args.steps):
+        r = cpu_reference_sample(cfg, seconds=max(3.0, 60.0 / max(1, args.warmup + args.steps)))
+        if k >= args.warmup:
+            per_step.append(r["value"])
+        cb = r
+    v = sum(per_step) / len(per_step)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": describe(name, cfg), "parallelism": "cpu"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"], "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------- our path
+def run_ours(args, cfg, name):
+    import torch
+    import torch.distributed as dist
+    from paper_2110_07663_b200 import semlab as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream(local)
+    torch.cuda.set_stream(stream)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [S.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = S.Context(local, stream, rank, world, uid[0])
+    else:
+        ctx = S.Context(local, stream)
+
+    sm = {"ras": S.RAS_SMOOTHER, "jacobi": S.JACOBI_SMOOTHER, "asm": S.ASM_SMOOTHER}[cfg["smoother"]]
+    cm = S.COARSE_AMG if cfg["coarse"] == "amg" else S.COARSE_DIRECT
+    t0 = time.time()
+    mesh = S.generate_kershaw(cfg["eps"], cfg["E"], ctx)
+    pmg = S.Pmg(mesh, cfg["orders"], sm, cfg["eta"], 0.1, 1.1, cfg["precision"], cm)
+    sp = pmg.spaces[0]
+    A, M = sp.as_linop(), pmg.as_linop()
+    solve = S.gmres_solve if cfg["krylov"] == "gmres" else S.pcg_solve
+    gcfg = S.GmresConfig(restart=20, tol=1e-8, max_iters=500)
+    b = sp.build_rhs(1)
+    x = torch.zeros_like(b)
+    setup_s = time.time() - t0
+    n_global = sp.n_global
+
+    def step():
+        x.zero_()
+        return solve(A, M, b, x, gcfg)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        st = step()
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = ctx.launch_count
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    conv = True
+    rel = 0.0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            st = step()
+            iters += st.iterations
+            conv = conv and st.converged
+            rel = max(rel, st.rel_residual)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = ctx.launch_count - launches0
+    t = ev0.elapsed_time(ev1) * 1e-3
+    if world > 1:
+        tt = torch.tensor([t], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = tt.item()
+    value = n_global * iters / t / 1e9
+
+    # end to end through the public API with HOST buffers (pinned): H2D of b, solve, D2H of x
+    hb = b.cpu().pin_memory()
+    hx = torch.empty_like(hb).pin_memory()
+    xb = torch.empty_like(b)
+    e2e_steps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    barrier()
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    it2 = 0
+    ev2.record(stream)
+    for _ in range(e2e_steps):
+        xb.copy_(hb, non_blocking=True)
+        x.zero_()
+        st = solve(A, M, xb, x, gcfg)
+        it2 += st.iterations
+        hx.copy_(x, non_blocking=True)
+    ev3.record(stream)
+    torch.cuda.synchronize()
+    t2 = ev2.elapsed_time(ev3) * 1e-3
+    if world > 1:
+        tt = torch.tensor([t2], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t2 = tt.item()
+    e2e = {"value": n_global * it2 / t2 / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * sp.n,
+           "d2h_bytes_per_step": 8 * sp.n, "steps": e2e_steps}
+
+    # roofline of the dominant kernel (fused Ax, global->global), timed live on its stream
+    pk = peaks()
+    u = torch.randn(sp.n, dtype=torch.float64, device="cuda")
+    w = torch.empty_like(u)
+    for _ in range(3):
+        sp.apply_A(u, w)
+    reps = 20
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e4.record(stream)
+    for _ in range(reps):
+        sp.apply_A(u, w)
+    e5.record(stream)
+    torch.cuda.synchronize()
+    t_ax = e4.elapsed_time(e5) * 1e-3 / reps
+    nloc = (cfg["p"] + 1) ** 3
+    ax_bytes = 48 * sp.n_elements * nloc + 16 * sp.n
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_summary.json")))
+        if prof.get("workload") == name:
+            traffic = prof.get("ax_dram_bytes_per_launch")
+    except Exception:
+        pass
+    peak = pk.get("hbm_gbs", 6650.0)
+    achieved = ax_bytes / t_ax / 1e9
+    roof = {"kernel": "k_ax (fused Ax + Q^T owner gather, global->global)", "bound": "hbm", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "algorithmic_bytes_per_launch": ax_bytes, "us_per_launch": t_ax * 1e6,
+            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in pk else "fallback"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(cfg, seconds=args.cpu_seconds)
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": describe(name, cfg), "n_dofs": n_global, "elements": cfg["E"] ** 3,
+                           "order": cfg["p"], "iterations_per_solve": iters / args.steps, "converged": conv,
+                           "max_rel_residual": rel, "smoother_precision": f"fp{cfg['precision']}",
+                           "krylov_precision": "fp64", "parallelism": f"z-slab x{world}", "setup_s": setup_s,
+                           "l2": "inputs larger than L2 (geometry 805 MB at E=32^3)",
+                           "time_to_1e-8_ms": t / args.steps * 1e3},
+                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
+                "gpu_launches": launches}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("timing rules: --warmup must be >= 3")
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, args.config)
+    else:
+        run_ours(args, cfg, args.config)
+
+
+if __name__ == "__main__":
+    main()
