@@ -58,6 +58,21 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Predicated L2 load (no branch: the load is simply not performed when !pred), 0.0 otherwise.
+__device__ __forceinline__ double ldcg_pred(const double* p, bool pred) {
+  double v = 0.0;
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.cg.f64 %0, [%1]; }"
+               : "+d"(v)
+               : "l"(p), "r"(int(pred)));
+  return v;
+}
+
 // Streaming (evict-first) loads for data touched once per sweep.
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 

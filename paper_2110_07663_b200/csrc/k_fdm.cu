@@ -1,16 +1,22 @@
 // Overlapping Schwarz smoother kernels (sm_100a), replacing SchwarzSmoother::apply and
 // fdm_solve (schwarz.cpp:228-289).
 //
-// One CTA per element. The extended box (order+3 per direction, padded; boundary elements are
-// smaller and padded with zero S rows) is extracted from the global lattice vector straight into
-// shared memory (sites outside the element core in more than one direction are zero-filled,
-// schwarz.cpp:255-265), transformed by S_x^T, S_y^T, S_z^T (one register-resident line per
-// thread, S broadcast from shared memory), scaled by inv_D = 1/(lx_i + ly_j + lz_k) recomputed
-// from the 3*(order+3) eigenvalues (schwarz.cpp:92-108; saves the (order+3)^3 table), and
-// transformed back. RAS: the element writes exactly the lattice nodes it owns (lowest element
-// whose core holds the node, schwarz.cpp:114-127) — a race-free owner write that can carry the
-// whole Chebyshev vector update. ASM: per-element boxes are written out and summed per node in
-// ascending element id (deterministic, the reference's order) then weighted by 1/count.
+// Several elements per CTA (order+3 = P per direction; boundary boxes are smaller and padded
+// with zero S rows). Each element's extended box is extracted from the global lattice vector
+// straight into shared memory (sites outside the element core in more than one direction are
+// zero-filled, schwarz.cpp:255-265). The three forward transforms S_x^T, S_y^T, S_z^T, the
+// scaling by inv_D = 1/(lx_i + ly_j + lz_k) (recomputed from the 3P eigenvalues instead of
+// streaming the P^3 table, schwarz.cpp:92-108) and the backward transforms run as line passes:
+// every thread keeps R lines of the box in registers and reads S as 2-wide vectors (one shared
+// load feeds 2R FMAs), so the passes are FMA-bound rather than shared-memory-bound.
+// RAS: the element writes exactly the lattice nodes it owns (lowest element whose core holds
+// the node, schwarz.cpp:114-127) — a race-free owner write that carries the whole Chebyshev
+// vector update. ASM: per-element boxes go to a buffer and every node sums the boxes covering it
+// in ascending element id (the reference's order) times 1/count (schwarz.cpp:269-287).
+#include <algorithm>
+#include <mutex>
+#include <unordered_set>
+
 #include "device.cuh"
 #include "kernels_fdm.hpp"
 
@@ -22,20 +28,17 @@ struct Box1D {  // extended-box geometry of one element along one axis (schwarz.
   int n, lo, gl, gr, own_lo, own_hi;  // own_*: box indices this element owns (RAS, inclusive)
 };
 
-__device__ __forceinline__ Box1D box1d(int e_d, int E_d, int q, bool dirichlet, int has_lower_rank,
-                                       int has_upper_rank) {
-  // has_*_rank: the neighbour element along this axis lives on another rank (z only)
+__device__ __forceinline__ Box1D box1d(int e_d, int E_d, int q, bool dirichlet) {
   Box1D b;
-  const bool left_int = e_d > 0 || has_lower_rank;
-  const bool right_int = e_d < E_d - 1 || has_upper_rank;
+  const bool left_int = e_d > 0;
+  const bool right_int = e_d < E_d - 1;
   const int i0 = (!left_int && dirichlet) ? 1 : 0;
   const int i1 = (!right_int && dirichlet) ? q - 1 : q;
   b.gl = left_int ? 1 : 0;
   b.gr = right_int ? 1 : 0;
   b.n = (i1 - i0 + 1) + b.gl + b.gr;
   b.lo = e_d * q + i0 - b.gl;
-  // owned element-local indices: [max(i0, left_int ? 1 : 0), i1]; box index a = i - i0 + gl
-  const int first = left_int ? 1 : i0;
+  const int first = left_int ? 1 : i0;  // the left face node is owned by the left neighbour
   b.own_lo = first - i0 + b.gl;
   b.own_hi = i1 - i0 + b.gl;
   return b;
@@ -43,175 +46,299 @@ __device__ __forceinline__ Box1D box1d(int e_d, int E_d, int q, bool dirichlet, 
 
 __device__ __forceinline__ bool ghost(const Box1D& b, int a) { return (b.gl && a == 0) || (b.gr && a == b.n - 1); }
 
-// out[a'] = sum_a M(a, a') in[a]  (transpose=true: S^T)  or  out[a] = sum_a' M(a, a') in[a'] (S)
-template <int P, class T, bool TRANS>
-__device__ __forceinline__ void line(const T* __restrict__ M /* P x P row-major M(a,a')=M[a*P+a'] */,
-                                     const T (&in)[P], T (&out)[P]) {
+template <int P, class T>
+struct Shape {
+  static constexpr int R = sizeof(T) == 4 ? 4 : 2;  // lines per thread
+  static constexpr int P2 = P * P, P3 = P2 * P;
+  static constexpr int TPE = (P2 + R - 1) / R;  // threads per element
+  static constexpr int NT = 128;
+  static constexpr int EPC = NT / TPE;  // elements per CTA
+  static constexpr int SPE = 2 * P3 + 3 * P2 + 3 * P + 2;  // smem T per element (even, 8B aligned)
+  static constexpr size_t smem() { return size_t(EPC) * SPE * sizeof(T); }
+};
+
+__device__ __forceinline__ float rcp(float s) { return __frcp_rn(s); }
+__device__ __forceinline__ double rcp(double s) { return 1.0 / s; }
+
+// One line pass along axis AX: for the thread's R lines, out = M^T in (FWD) or M in (!FWD);
+// MID: forward z, scale by inv_D, backward z in registers.
+template <int P, class T, int AX, int KIND /*0 fwd, 1 bwd, 2 mid*/>
+__device__ __forceinline__ void line_pass(const T* __restrict__ src, T* __restrict__ dst, const T* __restrict__ S,
+                                          const T* __restrict__ L, int ti) {
+  using Sh = Shape<P, T>;
+  constexpr int R = Sh::R, P2 = Sh::P2, TPE = Sh::TPE;
+  T in[R][P], out[R][P];
+  int base[R];
+  constexpr int stride = AX == 0 ? 1 : (AX == 1 ? P : P2);
 #pragma unroll
-  for (int o = 0; o < P; ++o) out[o] = T(0);
+  for (int r = 0; r < R; ++r) {
+    const int l = ti + TPE * r;
+    const int u = l % P, v = l / P;
+    base[r] = AX == 0 ? (v * P2 + u * P) : (AX == 1 ? (v * P2 + u) : (v * P + u));
+    const bool ok = l < P2;
 #pragma unroll
-  for (int a = 0; a < P; ++a) {
+    for (int m = 0; m < P; ++m) in[r][m] = ok ? src[base[r] + m * stride] : T(0);
+  }
+  auto fwd = [&](const T* M, T(&x)[R][P], T(&y)[R][P]) {  // y[o] = sum_a M(a,o) x[a]
 #pragma unroll
-    for (int o = 0; o < P; ++o) {
-      if (TRANS)
-        out[o] = fma(M[a * P + o], in[a], out[o]);
-      else
-        out[a] = fma(M[a * P + o], in[o], out[a]);
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int o = 0; o < P; ++o) y[r][o] = T(0);
+#pragma unroll
+    for (int a = 0; a < P; ++a) {
+      if constexpr (P % 2 == 0) {
+#pragma unroll
+        for (int o = 0; o < P; o += 2) {
+          T s0, s1;
+          if constexpr (sizeof(T) == 4) {
+            const float2 s = *reinterpret_cast<const float2*>(M + a * P + o);
+            s0 = s.x;
+            s1 = s.y;
+          } else {
+            const double2 s = *reinterpret_cast<const double2*>(M + a * P + o);
+            s0 = s.x;
+            s1 = s.y;
+          }
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            y[r][o] = fma(s0, x[r][a], y[r][o]);
+            y[r][o + 1] = fma(s1, x[r][a], y[r][o + 1]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int o = 0; o < P; ++o) {
+          const T s = M[a * P + o];
+#pragma unroll
+          for (int r = 0; r < R; ++r) y[r][o] = fma(s, x[r][a], y[r][o]);
+        }
+      }
+    }
+  };
+  auto bwd = [&](const T* M, T(&x)[R][P], T(&y)[R][P]) {  // y[a] = sum_o M(a,o) x[o]
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int a = 0; a < P; ++a) y[r][a] = T(0);
+#pragma unroll
+    for (int a = 0; a < P; ++a) {
+      if constexpr (P % 2 == 0) {
+#pragma unroll
+        for (int o = 0; o < P; o += 2) {
+          T s0, s1;
+          if constexpr (sizeof(T) == 4) {
+            const float2 s = *reinterpret_cast<const float2*>(M + a * P + o);
+            s0 = s.x;
+            s1 = s.y;
+          } else {
+            const double2 s = *reinterpret_cast<const double2*>(M + a * P + o);
+            s0 = s.x;
+            s1 = s.y;
+          }
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            y[r][a] = fma(s0, x[r][o], y[r][a]);
+            y[r][a] = fma(s1, x[r][o + 1], y[r][a]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int o = 0; o < P; ++o) {
+          const T s = M[a * P + o];
+#pragma unroll
+          for (int r = 0; r < R; ++r) y[r][a] = fma(s, x[r][o], y[r][a]);
+        }
+      }
+    }
+  };
+  if (KIND == 0) {
+    fwd(S, in, out);
+  } else if (KIND == 1) {
+    bwd(S, in, out);
+  } else {
+    fwd(S, in, out);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int l = ti + TPE * r;
+      const int a = l % P, b = (l / P) % P;
+      const T lab = L[0 * P + a] + L[1 * P + b];
+#pragma unroll
+      for (int c = 0; c < P; ++c) out[r][c] = out[r][c] * rcp(lab + L[2 * P + c]);
+    }
+    bwd(S, out, in);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int m = 0; m < P; ++m) out[r][m] = in[r][m];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int l = ti + TPE * r;
+    if (l < P2)
+#pragma unroll
+      for (int m = 0; m < P; ++m) dst[base[r] + m * stride] = out[r][m];
+  }
+}
+
+// Block of EPC elements: load factors + boxes (from the lattice vector or from a box array),
+// run the five line passes. Result left in the element's tmp buffer.
+template <int P, class T, bool FROM_BOXES>
+__device__ __forceinline__ void fdm_block(const Slab& sl, const T* __restrict__ S, const T* __restrict__ L,
+                                          const double* __restrict__ src, int64_t e_first, int64_t nE, T* smem,
+                                          Box1D (*bx)[3]) {
+  using Sh = Shape<P, T>;
+  constexpr int P2 = Sh::P2, P3 = Sh::P3, EPC = Sh::EPC, SPE = Sh::SPE, TPE = Sh::TPE;
+  const int tid = threadIdx.x;
+  if (!FROM_BOXES && tid < EPC) {
+    const int64_t el = e_first + tid;
+    if (el < nE) {
+      const int ex = int(el % sl.Ex), ey = int((el / sl.Ex) % sl.Ey);
+      const int ez = sl.ez0 + int(el / (int64_t(sl.Ex) * sl.Ey));
+      const bool dir = sl.dirichlet != 0;
+      bx[tid][0] = box1d(ex, sl.Ex, sl.q, dir);
+      bx[tid][1] = box1d(ey, sl.Ey, sl.q, dir);
+      bx[tid][2] = box1d(ez, sl.Ez, sl.q, dir);
     }
   }
-}
-
-// Apply the box solve in shared memory: box[c][b][a] (P^3, stride P) -> box (in place via tmp).
-template <int P, class T>
-__device__ void fdm_box(T* __restrict__ box, T* __restrict__ tmp, const T* __restrict__ sS, const T* __restrict__ sL,
-                        int tid, int nthreads) {
-  constexpr int P2 = P * P;
-  T in[P], out[P];
-  // x: S_x^T along a, lines (b,c)
-  for (int l = tid; l < P2; l += nthreads) {
-    const int b = l % P, c = l / P;
+  // factors: S (3 P^2) and lambda (3 P) of each element; all loads issued before the stores
+  {
+    constexpr int NF = 3 * P2 + 3 * P, ITER = (EPC * NF + Sh::NT - 1) / Sh::NT;
+    T v[ITER];
 #pragma unroll
-    for (int a = 0; a < P; ++a) in[a] = box[c * P2 + b * P + a];
-    line<P, T, true>(sS + 0 * P2, in, out);
+    for (int it = 0; it < ITER; ++it) {
+      const int t = tid + it * Sh::NT;
+      const int e = t / NF, w = t % NF;
+      const int64_t el = e_first + e;
+      const bool ok = t < EPC * NF && el < nE;
+      v[it] = !ok ? T(0) : (w < 3 * P2 ? __ldg(S + el * 3 * P2 + w) : __ldg(L + el * 3 * P + (w - 3 * P2)));
+    }
 #pragma unroll
-    for (int a = 0; a < P; ++a) tmp[c * P2 + b * P + a] = out[a];
+    for (int it = 0; it < ITER; ++it) {
+      const int t = tid + it * Sh::NT;
+      if (t < EPC * NF) smem[(t / NF) * SPE + 2 * P3 + t % NF] = v[it];
+    }
   }
   __syncthreads();
-  // y: S_y^T along b, lines (a,c)
-  for (int l = tid; l < P2; l += nthreads) {
-    const int a = l % P, c = l / P;
+  // extraction by box rows (b,c): the P loads of a row are independent and issued together
+  for (int rr = tid; rr < EPC * P2; rr += Sh::NT) {
+    const int e = rr / P2, w = rr % P2, b = w % P, c = w / P;
+    const int64_t el = e_first + e;
+    T v[P];
+    if (FROM_BOXES) {
 #pragma unroll
-    for (int b = 0; b < P; ++b) in[b] = tmp[c * P2 + b * P + a];
-    line<P, T, true>(sS + 1 * P2, in, out);
+      for (int a = 0; a < P; ++a) v[a] = el < nE ? T(src[el * P3 + w * P + a]) : T(0);
+    } else {
+      const Box1D &X = bx[e][0], &Y = bx[e][1], &Z = bx[e][2];
+      const bool row_ok = el < nE && b < Y.n && c < Z.n;
+      const int gyz = row_ok ? int(ghost(Y, b)) + int(ghost(Z, c)) : 2;
+      const double* rowp = src + (row_ok ? sl.lidx(X.lo, Y.lo + b, Z.lo + c) : 0);
+      // unconditional loads from always-valid (clamped) addresses, then select: no branch
+      // per load, so all P loads of the row are in flight together
 #pragma unroll
-    for (int b = 0; b < P; ++b) box[c * P2 + b * P + a] = out[b];
+      for (int a = 0; a < P; ++a) {
+        const bool ok = row_ok && a < X.n && gyz + int(ghost(X, a)) <= 1;
+        const double val = __ldg(rowp + (a < X.n ? a : 0));
+        v[a] = ok ? T(val) : T(0);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < P; ++a) smem[e * SPE + w * P + a] = v[a];
   }
   __syncthreads();
-  // z: S_z^T along c, scale by inv_D, then S_z back (lines (a,b))
-  for (int l = tid; l < P2; l += nthreads) {
-    const int a = l % P, b = l / P;
-#pragma unroll
-    for (int c = 0; c < P; ++c) in[c] = box[c * P2 + b * P + a];
-    line<P, T, true>(sS + 2 * P2, in, out);
-    const T lab = sL[0 * P + a] + sL[1 * P + b];
-#pragma unroll
-    for (int c = 0; c < P; ++c) out[c] = out[c] / (lab + sL[2 * P + c]);
-    line<P, T, false>(sS + 2 * P2, out, in);
-#pragma unroll
-    for (int c = 0; c < P; ++c) box[c * P2 + b * P + a] = in[c];
-  }
+  const int e = tid / TPE, ti = tid % TPE;
+  const bool act = e < EPC && e_first + e < nE;
+  T* box = smem + (act ? e : 0) * SPE;
+  T* tmp = box + P3;
+  const T* Se = box + 2 * P3;
+  const T* Le = Se + 3 * P2;
+  if (act) line_pass<P, T, 0, 0>(box, tmp, Se + 0 * P2, Le, ti);
   __syncthreads();
-  // y back
-  for (int l = tid; l < P2; l += nthreads) {
-    const int a = l % P, c = l / P;
-#pragma unroll
-    for (int b = 0; b < P; ++b) in[b] = box[c * P2 + b * P + a];
-    line<P, T, false>(sS + 1 * P2, in, out);
-#pragma unroll
-    for (int b = 0; b < P; ++b) tmp[c * P2 + b * P + a] = out[b];
-  }
+  if (act) line_pass<P, T, 1, 0>(tmp, box, Se + 1 * P2, Le, ti);
   __syncthreads();
-  // x back
-  for (int l = tid; l < P2; l += nthreads) {
-    const int b = l % P, c = l / P;
-#pragma unroll
-    for (int a = 0; a < P; ++a) in[a] = tmp[c * P2 + b * P + a];
-    line<P, T, false>(sS + 0 * P2, in, out);
-#pragma unroll
-    for (int a = 0; a < P; ++a) box[c * P2 + b * P + a] = out[a];
-  }
+  if (act) line_pass<P, T, 2, 2>(box, tmp, Se + 2 * P2, Le, ti);
   __syncthreads();
-}
-
-template <int P, class T>
-__device__ __forceinline__ void load_factors(const T* __restrict__ S, const T* __restrict__ L, int64_t el, T* sS, T* sL,
-                                             int tid, int nthreads) {
-  const T* Se = S + el * 3 * P * P;
-  for (int t = tid; t < 3 * P * P; t += nthreads) sS[t] = Se[t];
-  const T* Le = L + el * 3 * P;
-  for (int t = tid; t < 3 * P; t += nthreads) sL[t] = Le[t];
+  if (act) line_pass<P, T, 1, 1>(tmp, box, Se + 1 * P2, Le, ti);
+  __syncthreads();
+  if (act) line_pass<P, T, 0, 1>(box, tmp, Se + 0 * P2, Le, ti);
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- RAS (+ fused Chebyshev update)
 template <int P, class T, int MODE>
-__global__ void __launch_bounds__(128) k_ras(const Slab sl, const T* __restrict__ S, const T* __restrict__ L,
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_ras(const Slab sl, const T* __restrict__ S, const T* __restrict__ L,
                                              const double* __restrict__ r, RasEpi epi) {
-  constexpr int P2 = P * P, P3 = P2 * P;
-  __shared__ T sS[3 * P2];
-  __shared__ T sL[3 * P];
-  __shared__ T box[P3];
-  __shared__ T tmp[P3];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t el = blockIdx.x;
-  const int q = sl.q;
-  const int ex = int(el % sl.Ex), ey = int((el / sl.Ex) % sl.Ey), ez = sl.ez0 + int(el / (int64_t(sl.Ex) * sl.Ey));
-  const bool dir = sl.dirichlet != 0;
-  const Box1D bx = box1d(ex, sl.Ex, q, dir, 0, 0);
-  const Box1D by = box1d(ey, sl.Ey, q, dir, 0, 0);
-  const Box1D bz = box1d(ez, sl.Ez, q, dir, 0, 0);
-  load_factors<P, T>(S, L, el, sS, sL, tid, nt);
-  for (int t = tid; t < P3; t += nt) {
-    const int a = t % P, b = (t / P) % P, c = t / P2;
-    T v = T(0);
-    if (a < bx.n && b < by.n && c < bz.n) {
-      const int out = int(ghost(bx, a)) + int(ghost(by, b)) + int(ghost(bz, c));
-      if (out <= 1) v = T(r[sl.lidx(bx.lo + a, by.lo + b, bz.lo + c)]);
-    }
-    box[t] = v;
-  }
-  __syncthreads();
-  fdm_box<P, T>(box, tmp, sS, sL, tid, nt);
-  const int wa = bx.own_hi - bx.own_lo + 1, wb = by.own_hi - by.own_lo + 1, wc = bz.own_hi - bz.own_lo + 1;
-  for (int t = tid; t < wa * wb * wc; t += nt) {
-    const int a = bx.own_lo + t % wa, b = by.own_lo + (t / wa) % wb, c = bz.own_lo + t / (wa * wb);
-    const int64_t g = sl.lidx(bx.lo + a, by.lo + b, bz.lo + c);
-    const double z = double(box[c * P2 + b * P + a]);
+  using Sh = Shape<P, T>;
+  constexpr int P2 = Sh::P2, P3 = Sh::P3, EPC = Sh::EPC, SPE = Sh::SPE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  __shared__ Box1D bx[EPC][3];
+  const int64_t nE = sl.elems();
+  const int64_t e_first = int64_t(blockIdx.x) * EPC;
+  fdm_block<P, T, false>(sl, S, L, r, e_first, nE, smem, bx);
+  // owner write by rows of owned sites (all vector loads of a row issued together)
+  constexpr int Q = P - 3;  // order: at most Q owned sites per direction
+  for (int rr = threadIdx.x; rr < EPC * Q * Q; rr += Sh::NT) {
+    const int e = rr / (Q * Q), w = rr % (Q * Q);
+    if (e_first + e >= nE) continue;
+    const Box1D &X = bx[e][0], &Y = bx[e][1], &Z = bx[e][2];
+    const int wa = X.own_hi - X.own_lo + 1, wb = Y.own_hi - Y.own_lo + 1, wc = Z.own_hi - Z.own_lo + 1;
+    if (w >= wb * wc) continue;
+    const int b = Y.own_lo + w % wb, c = Z.own_lo + w / wb;
+    const int64_t g0 = sl.lidx(X.lo + X.own_lo, Y.lo + b, Z.lo + c);
+    const T* zrow = smem + e * SPE + P3 + c * P2 + b * P + X.own_lo;
     if (MODE == 0) {
-      epi.out[g] = z;
+#pragma unroll
+      for (int a = 0; a < Q; ++a)
+        if (a < wa) epi.out[g0 + a] = double(zrow[a]);
     } else if (MODE == 1) {  // Chebyshev init: r = S t, d = r / theta  (chebyshev.cpp:82-84)
-      epi.r[g] = z;
-      epi.d[g] = z / epi.c1;
+#pragma unroll
+      for (int a = 0; a < Q; ++a)
+        if (a < wa) {
+          const double z = double(zrow[a]);
+          epi.r[g0 + a] = z;
+          epi.d[g0 + a] = z / epi.c1;
+        }
     } else {  // Chebyshev step: x += d; r -= S A d; d = c1 d + c2 r  (chebyshev.cpp:86-92)
-      const double dg = epi.d[g];
-      epi.x[g] += dg;
-      const double rg = epi.r[g] - z;
-      epi.r[g] = rg;
-      epi.d[g] = epi.c1 * dg + epi.c2 * rg;
+      double dv[Q], rv[Q], xv[Q];
+#pragma unroll
+      for (int a = 0; a < Q; ++a) {
+        const int64_t ga = g0 + (a < wa ? a : 0);  // clamped: loads are unconditional
+        dv[a] = epi.d[ga];
+        rv[a] = epi.r[ga];
+        xv[a] = epi.x[ga];
+      }
+#pragma unroll
+      for (int a = 0; a < Q; ++a)
+        if (a < wa) {
+          const double z = double(zrow[a]);
+          epi.x[g0 + a] = xv[a] + dv[a];
+          const double rg = rv[a] - z;
+          epi.r[g0 + a] = rg;
+          epi.d[g0 + a] = epi.c1 * dv[a] + epi.c2 * rg;
+        }
     }
   }
 }
 
 // ---------------------------------------------------------------- ASM boxes + deterministic sum
 template <int P, class T>
-__global__ void __launch_bounds__(128) k_asm_boxes(const Slab sl, const T* __restrict__ S, const T* __restrict__ L,
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_asm_boxes(const Slab sl, const T* __restrict__ S, const T* __restrict__ L,
                                                    const double* __restrict__ r, T* __restrict__ boxes) {
-  constexpr int P2 = P * P, P3 = P2 * P;
-  __shared__ T sS[3 * P2];
-  __shared__ T sL[3 * P];
-  __shared__ T box[P3];
-  __shared__ T tmp[P3];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t el = blockIdx.x;
-  const int q = sl.q;
-  const int ex = int(el % sl.Ex), ey = int((el / sl.Ex) % sl.Ey), ez = sl.ez0 + int(el / (int64_t(sl.Ex) * sl.Ey));
-  const bool dir = sl.dirichlet != 0;
-  const Box1D bx = box1d(ex, sl.Ex, q, dir, 0, 0), by = box1d(ey, sl.Ey, q, dir, 0, 0), bz = box1d(ez, sl.Ez, q, dir, 0, 0);
-  load_factors<P, T>(S, L, el, sS, sL, tid, nt);
-  for (int t = tid; t < P3; t += nt) {
-    const int a = t % P, b = (t / P) % P, c = t / P2;
-    T v = T(0);
-    if (a < bx.n && b < by.n && c < bz.n) {
-      const int out = int(ghost(bx, a)) + int(ghost(by, b)) + int(ghost(bz, c));
-      if (out <= 1) v = T(r[sl.lidx(bx.lo + a, by.lo + b, bz.lo + c)]);
-    }
-    box[t] = v;
+  using Sh = Shape<P, T>;
+  constexpr int P3 = Sh::P3, EPC = Sh::EPC, SPE = Sh::SPE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  __shared__ Box1D bx[EPC][3];
+  const int64_t nE = sl.elems();
+  const int64_t e_first = int64_t(blockIdx.x) * EPC;
+  fdm_block<P, T, false>(sl, S, L, r, e_first, nE, smem, bx);
+  for (int t = threadIdx.x; t < EPC * P3; t += Sh::NT) {
+    const int e = t / P3, w = t % P3;
+    if (e_first + e < nE) boxes[(e_first + e) * P3 + w] = smem[e * SPE + P3 + w];
   }
-  __syncthreads();
-  fdm_box<P, T>(box, tmp, sS, sL, tid, nt);
-  for (int t = tid; t < P3; t += nt) boxes[el * P3 + t] = box[t];
 }
 
-// out[g] = w(g) * sum over elements whose participating box covers g (ascending id), w = 1/count
+// out[g] = (1/count) * sum over elements whose participating box covers g, ascending id
 template <int P, class T>
 __global__ void k_asm_sum(const Slab sl, const T* __restrict__ boxes, double* __restrict__ out) {
   constexpr int P2 = P * P, P3 = P2 * P;
@@ -221,7 +348,6 @@ __global__ void k_asm_sum(const Slab sl, const T* __restrict__ boxes, double* __
   const int64_t total = sl.Nx * sl.Ny * nz;
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
     const int64_t x = t % sl.Nx, y = (t / sl.Nx) % sl.Ny, z = z0 + t / (sl.Nx * sl.Ny);
-    // candidate elements per axis: at most two boxes cover a lattice coordinate
     int ce[3][3], ca[3][3], cg[3][3], cn[3] = {0, 0, 0};
     const int64_t coord[3] = {x, y, z};
     const int Ed[3] = {sl.Ex, sl.Ey, sl.Ez};
@@ -230,7 +356,7 @@ __global__ void k_asm_sum(const Slab sl, const T* __restrict__ boxes, double* __
       const int base = int(coord[d] / q);
       for (int e = base - 1; e <= base + 1; ++e) {
         if (e < lo_e[d] || e >= hi_e[d]) continue;
-        const Box1D b = box1d(e, Ed[d], q, dir, 0, 0);
+        const Box1D b = box1d(e, Ed[d], q, dir);
         const int a = int(coord[d]) - b.lo;
         if (a < 0 || a >= b.n) continue;
         ce[d][cn[d]] = e;
@@ -255,56 +381,78 @@ __global__ void k_asm_sum(const Slab sl, const T* __restrict__ boxes, double* __
 
 // fdm_solve on given boxes (API / tests), FP64 in/out
 template <int P, class T>
-__global__ void __launch_bounds__(128) k_fdm_boxes(const T* __restrict__ S, const T* __restrict__ L,
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_fdm_boxes(const Slab sl, const T* __restrict__ S, const T* __restrict__ L,
                                                    const double* __restrict__ in, double* __restrict__ outb) {
-  constexpr int P2 = P * P, P3 = P2 * P;
-  __shared__ T sS[3 * P2];
-  __shared__ T sL[3 * P];
-  __shared__ T box[P3];
-  __shared__ T tmp[P3];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t el = blockIdx.x;
-  load_factors<P, T>(S, L, el, sS, sL, tid, nt);
-  for (int t = tid; t < P3; t += nt) box[t] = T(in[el * P3 + t]);
-  __syncthreads();
-  fdm_box<P, T>(box, tmp, sS, sL, tid, nt);
-  for (int t = tid; t < P3; t += nt) outb[el * P3 + t] = double(box[t]);
+  using Sh = Shape<P, T>;
+  constexpr int P3 = Sh::P3, EPC = Sh::EPC, SPE = Sh::SPE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  __shared__ Box1D bx[EPC][3];
+  const int64_t nE = sl.elems();
+  const int64_t e_first = int64_t(blockIdx.x) * EPC;
+  fdm_block<P, T, true>(sl, S, L, in, e_first, nE, smem, bx);
+  for (int t = threadIdx.x; t < EPC * P3; t += Sh::NT) {
+    const int e = t / P3, w = t % P3;
+    if (e_first + e < nE) outb[(e_first + e) * P3 + w] = double(smem[e * SPE + P3 + w]);
+  }
+}
+
+template <class K>
+void prep(K kern, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert(reinterpret_cast<const void*>(kern)).second)
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
 }
 
 template <class T>
 struct Launch {
   template <int P>
   static void ras(const Slab& sl, const T* S, const T* L, const double* r, int mode, const RasEpi& e, cudaStream_t s) {
-    const int grid = int(sl.elems());
-    if (mode == 0) k_ras<P, T, 0><<<grid, 128, 0, s>>>(sl, S, L, r, e);
-    else if (mode == 1) k_ras<P, T, 1><<<grid, 128, 0, s>>>(sl, S, L, r, e);
-    else k_ras<P, T, 2><<<grid, 128, 0, s>>>(sl, S, L, r, e);
+    using Sh = Shape<P, T>;
+    const int grid = int((sl.elems() + Sh::EPC - 1) / Sh::EPC);
+    if (mode == 0) {
+      prep(k_ras<P, T, 0>, Sh::smem());
+      k_ras<P, T, 0><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, r, e);
+    } else if (mode == 1) {
+      prep(k_ras<P, T, 1>, Sh::smem());
+      k_ras<P, T, 1><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, r, e);
+    } else {
+      prep(k_ras<P, T, 2>, Sh::smem());
+      k_ras<P, T, 2><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, r, e);
+    }
   }
   template <int P>
   static void asm_(const Slab& sl, const T* S, const T* L, const double* r, void* boxes, double* out, cudaStream_t s) {
-    k_asm_boxes<P, T><<<int(sl.elems()), 128, 0, s>>>(sl, S, L, r, static_cast<T*>(boxes));
+    using Sh = Shape<P, T>;
+    const int grid = int((sl.elems() + Sh::EPC - 1) / Sh::EPC);
+    prep(k_asm_boxes<P, T>, Sh::smem());
+    k_asm_boxes<P, T><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, r, static_cast<T*>(boxes));
     const int64_t total = sl.Nx * sl.Ny * (int64_t(sl.ez1 - sl.ez0) * sl.q + 1);
     k_asm_sum<P, T><<<int(std::min<int64_t>((total + 255) / 256, 148 * 32)), 256, 0, s>>>(
         sl, static_cast<const T*>(boxes), out);
   }
   template <int P>
-  static void boxes(int64_t E, const T* S, const T* L, const double* in, double* out, cudaStream_t s) {
-    k_fdm_boxes<P, T><<<int(E), 128, 0, s>>>(S, L, in, out);
+  static void boxes(const Slab& sl, const T* S, const T* L, const double* in, double* out, cudaStream_t s) {
+    using Sh = Shape<P, T>;
+    const int grid = int((sl.elems() + Sh::EPC - 1) / Sh::EPC);
+    prep(k_fdm_boxes<P, T>, Sh::smem());
+    k_fdm_boxes<P, T><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, in, out);
   }
 };
 
-#define SB_FDM_SWITCH(P_, CALL)                                                     \
-  switch (P_) {                                                                      \
-    case 4: CALL(4); break;                                                          \
-    case 5: CALL(5); break;                                                          \
-    case 6: CALL(6); break;                                                          \
-    case 7: CALL(7); break;                                                          \
-    case 8: CALL(8); break;                                                          \
-    case 9: CALL(9); break;                                                          \
-    case 10: CALL(10); break;                                                        \
-    case 11: CALL(11); break;                                                        \
-    case 12: CALL(12); break;                                                        \
-    default: invalid("SchwarzSmoother: device kernels support orders 1..9");        \
+#define SB_FDM_SWITCH(P_, CALL)                                              \
+  switch (P_) {                                                               \
+    case 5: CALL(5); break;                                                   \
+    case 6: CALL(6); break;                                                   \
+    case 7: CALL(7); break;                                                   \
+    case 8: CALL(8); break;                                                   \
+    case 9: CALL(9); break;                                                   \
+    case 10: CALL(10); break;                                                 \
+    case 11: CALL(11); break;                                                 \
+    case 12: CALL(12); break;                                                 \
+    default: invalid("SchwarzSmoother: device kernels support orders 2..9"); \
   }
 
 }  // namespace
@@ -343,16 +491,16 @@ int64_t launch_asm(const Slab& sl, int precision, const void* S, const void* L, 
   return 2;
 }
 
-int64_t launch_fdm_boxes(int q, int64_t E, int precision, const void* S, const void* L, const double* in, double* out,
+int64_t launch_fdm_boxes(const Slab& sl, int precision, const void* S, const void* L, const double* in, double* out,
                          cudaStream_t s) {
-  if (E == 0) return 0;
-  const int P = q + 3;
+  if (sl.elems() == 0) return 0;
+  const int P = sl.q + 3;
   if (precision == 32) {
-#define C32(PP) Launch<float>::boxes<PP>(E, static_cast<const float*>(S), static_cast<const float*>(L), in, out, s)
+#define C32(PP) Launch<float>::boxes<PP>(sl, static_cast<const float*>(S), static_cast<const float*>(L), in, out, s)
     SB_FDM_SWITCH(P, C32)
 #undef C32
   } else {
-#define C64(PP) Launch<double>::boxes<PP>(E, static_cast<const double*>(S), static_cast<const double*>(L), in, out, s)
+#define C64(PP) Launch<double>::boxes<PP>(sl, static_cast<const double*>(S), static_cast<const double*>(L), in, out, s)
     SB_FDM_SWITCH(P, C64)
 #undef C64
   }

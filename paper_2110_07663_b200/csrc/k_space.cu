@@ -146,19 +146,22 @@ __global__ void k_geom(const Slab sl, const DMat<ND> Dm, const W1<ND> w1, const 
 }
 
 // ------------------------------------------------------------------------ Ax
+template <int ND>
+constexpr int ax_min_blocks() {  // occupancy target: caps registers so ~20 warps/SM stay resident
+  return ND >= 8 ? 10 : 4;
+}
+
 template <int ND, int EPB, bool LOCAL, class EpiT>
-__global__ void __launch_bounds__(EPB* ND* ND)
+__global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
     k_ax(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const double* __restrict__ geom,
          double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int ngroups,
          double* __restrict__ out_local, const EpiT epi) {
   constexpr int ND2 = ND * ND, NLOC = ND2 * ND, NT = EPB * ND2;
   constexpr int q = ND - 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* s_geom = reinterpret_cast<double*>(smem_raw);
-  double* s_a = s_geom + EPB * 6 * NLOC;
+  double* s_a = reinterpret_cast<double*>(smem_raw);
   double* s_b = s_a + EPB * NLOC;
   double* s_D = s_b + EPB * NLOC;
-  __shared__ __align__(8) uint64_t bar;
   __shared__ int s_grp;
   __shared__ unsigned s_epoch;
   const int tid = threadIdx.x;
@@ -172,7 +175,6 @@ __global__ void __launch_bounds__(EPB* ND* ND)
       if (t == ngroups - 1) atomicExch(ticket, 0u);  // every ticket of this launch is taken
     }
     s_grp = t;
-    mbar_init(&bar, 1);
   }
   for (int t = tid; t < ND2; t += NT) s_D[t] = Dm.d[t];
   __syncthreads();
@@ -180,12 +182,13 @@ __global__ void __launch_bounds__(EPB* ND* ND)
   const int64_t nE = sl.elems();
   const int64_t e0 = int64_t(s_grp) * EPB;
   const int ne = int(nE - e0 < EPB ? nE - e0 : EPB);
-  if (tid == 0) {
-    const unsigned bytes = unsigned(ne) * 6u * NLOC * unsigned(sizeof(double));
-    mbar_expect_tx(&bar, bytes);
-    bulk_g2s(s_geom, geom + e0 * 6 * NLOC, bytes, &bar);
-    if (!LOCAL) s_epoch = *reinterpret_cast<volatile unsigned*>(&flags[e0]);
+  {  // stream the group's geometry (contiguous, 48 B/node) into L2 while u is loaded and
+     // differentiated; phase 2 then reads it at L2 latency without holding shared memory
+    const char* gbase = reinterpret_cast<const char*>(geom + e0 * 6 * NLOC);
+    const int lines = (ne * 6 * NLOC * int(sizeof(double)) + 127) / 128;
+    for (int l = tid; l < lines; l += NT) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + size_t(l) * 128));
   }
+  if (tid == 0 && !LOCAL) s_epoch = *reinterpret_cast<volatile unsigned*>(&flags[e0]);
 
   const int le = tid / ND2, ij = tid % ND2, i = ij % ND, j = ij / ND;
   const bool active = le < ne;
@@ -199,51 +202,54 @@ __global__ void __launch_bounds__(EPB* ND* ND)
   // phase 0: u column (i,j,:) into registers and the element block into smem
   double ureg[ND];
 #pragma unroll
-  for (int k = 0; k < ND; ++k) {
-    double v = 0.0;
-    if (active) {
-      if (LOCAL)
-        v = u[el * NLOC + k * ND2 + ij];
-      else
-        v = sl.masked(x, y, zb + k) ? 0.0 : __ldg(&u[sl.lidx(x, y, zb + k)]);
-    }
+  for (int k = 0; k < ND; ++k) {  // unconditional loads (el is clamped to a valid element), then select
+    const double raw = LOCAL ? __ldg(&u[el * NLOC + k * ND2 + ij]) : __ldg(&u[sl.lidx(x, y, zb + k)]);
+    const double v = (!active || (!LOCAL && sl.masked(x, y, zb + k))) ? 0.0 : raw;
     ureg[k] = v;
     sa[k * ND2 + ij] = v;
   }
   __syncthreads();
-  double Di[ND], Dj[ND], DiT[ND], DjT[ND];
-#pragma unroll
-  for (int m = 0; m < ND; ++m) {
-    Di[m] = s_D[i + ND * m];
-    Dj[m] = s_D[j + ND * m];
-    DiT[m] = s_D[m + ND * i];
-    DjT[m] = s_D[m + ND * j];
-  }
 
   // phase 1: ur, us, ut (sem_space.cpp:137-151)
   double ur[ND], us[ND], ut[ND];
-#pragma unroll
-  for (int k = 0; k < ND; ++k) {
-    double dr = 0.0, ds = 0.0, dt = 0.0;
+  {
+    double Di[ND], Dj[ND];
 #pragma unroll
     for (int m = 0; m < ND; ++m) {
-      dr = fma(Di[m], sa[k * ND2 + j * ND + m], dr);
-      ds = fma(Dj[m], sa[k * ND2 + m * ND + i], ds);
-      dt = fma(Dm.d[k + ND * m], ureg[m], dt);
+      Di[m] = s_D[i + ND * m];
+      Dj[m] = s_D[j + ND * m];
     }
-    ur[k] = dr;
-    us[k] = ds;
-    ut[k] = dt;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      double dr = 0.0, ds = 0.0, dt = 0.0;
+#pragma unroll
+      for (int m = 0; m < ND; ++m) {
+        dr = fma(Di[m], sa[k * ND2 + j * ND + m], dr);
+        ds = fma(Dj[m], sa[k * ND2 + m * ND + i], ds);
+        dt = fma(Dm.d[k + ND * m], ureg[m], dt);
+      }
+      ur[k] = dr;
+      us[k] = ds;
+      ut[k] = dt;
+    }
   }
 
-  // phase 2: geometric factors (sem_space.cpp:153-161)
-  mbar_wait(&bar, 0);
-  const double* gg = s_geom + le * 6 * NLOC;
+  // phase 2: geometric factors (sem_space.cpp:153-161), read from L2 (prefetched above)
+  const double* gg = geom + el * 6 * NLOC + ij;
 #pragma unroll
   for (int k = 0; k < ND; ++k) {
-    const int node = k * ND2 + ij;
-    const double g0 = gg[0 * NLOC + node], g1 = gg[1 * NLOC + node], g2 = gg[2 * NLOC + node];
-    const double g3 = gg[3 * NLOC + node], g4 = gg[4 * NLOC + node], g5 = gg[5 * NLOC + node];
+    // per-layer guarded loads: keeps the 6*ND geometry loads from all being hoisted at once
+    // (that spills at the 96-register occupancy target); the geometry sits in L2 (prefetched)
+    const int node = k * ND2;
+    double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0;
+    if (active) {
+      g0 = __ldcs(gg + 0 * NLOC + node);
+      g1 = __ldcs(gg + 1 * NLOC + node);
+      g2 = __ldcs(gg + 2 * NLOC + node);
+      g3 = __ldcs(gg + 3 * NLOC + node);
+      g4 = __ldcs(gg + 4 * NLOC + node);
+      g5 = __ldcs(gg + 5 * NLOC + node);
+    }
     const double r = ur[k], s = us[k], t = ut[k];
     ur[k] = g0 * r + g1 * s + g2 * t;
     us[k] = g1 * r + g3 * s + g4 * t;
@@ -258,6 +264,12 @@ __global__ void __launch_bounds__(EPB* ND* ND)
   __syncthreads();
 
   // phase 3: transposed contractions, interleaved in one accumulator (sem_space.cpp:163-174)
+  double DiT[ND], DjT[ND];
+#pragma unroll
+  for (int m = 0; m < ND; ++m) {
+    DiT[m] = s_D[m + ND * i];
+    DjT[m] = s_D[m + ND * j];
+  }
   double out[ND];
 #pragma unroll
   for (int k = 0; k < ND; ++k) {
@@ -289,7 +301,8 @@ __global__ void __launch_bounds__(EPB* ND* ND)
       if (!own) dep[el * NLOC + k * ND2 + ij] = out[k];
     }
   }
-  __threadfence();
+  // CTA barrier then one gpu-scope release per element: the release is cumulative over the
+  // deposits the barrier ordered before it (the CUTLASS semaphore pattern).
   __syncthreads();
   const unsigned target = s_epoch + 1u;
   if (tid < ne) st_release(&flags[e0 + tid], target);
@@ -302,33 +315,56 @@ __global__ void __launch_bounds__(EPB* ND* ND)
       const int a = combo & 1, b = (combo >> 1) & 1, c = (combo >> 2) & 1;
       if ((!a || wx > 0) && (!b || wy > 0) && (!c || wz > sl.ez0)) {
         const int64_t nb = we - a - int64_t(b) * sl.Ex - int64_t(c) * sl.Ex * sl.Ey;
-        while (ld_acquire(&flags[nb]) < target) __nanosleep(32);
+        // relaxed spin: the deposits are read with ld.global.cg from L2 (the coherence point)
+        // after the flag is observed, so no L1-invalidating acquire is needed
+        while (ld_relaxed(&flags[nb]) < target) __nanosleep(32);
       }
     }
   }
   __syncthreads();
   if (!active) return;
 
-  // phase 5: owned nodes summed in ascending element id (sem_space.cpp:113-117 order)
-  const int amax = (i == 0 && ex > 0) ? 1 : 0;
-  const int bmax = (j == 0 && ey > 0) ? 1 : 0;
+  // phase 5: owned nodes summed in ascending element id (sem_space.cpp:113-117 order). All
+  // deposit loads are issued up front (predicated, unrolled) so they cost one L2 round trip;
+  // absent contributors add an exact 0.0, which leaves the reference's sum bitwise unchanged.
+  const bool hx = (i == 0 && ex > 0), hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
+  const int64_t LX = 1, LY = sl.Ex, LZ = int64_t(sl.Ex) * sl.Ey;
+  const double* dbase = dep + el * NLOC + ij;
+  const bool own0 = ownx && owny && hz;
+  const double cz = ldcg_pred(dbase - LZ * NLOC + q * ND2, own0);
+  const double cxz = ldcg_pred(dbase - (LZ + LX) * NLOC + q * ND2 + q, own0 && hx);
+  const double cyz = ldcg_pred(dbase - (LZ + LY) * NLOC + q * ND2 + q * ND, own0 && hy);
+  const double cxyz = ldcg_pred(dbase - (LZ + LY + LX) * NLOC + q * ND2 + q * ND + q, own0 && hx && hy);
+  constexpr int KH = (ND + 1) / 2;  // two batches of layers bound the live registers
 #pragma unroll
-  for (int k = 0; k < ND; ++k) {
-    if (!(ownx && owny && (k < q || topz))) continue;
-    const int cmax = (k == 0 && ez > sl.ez0) ? 1 : 0;
-    double acc = 0.0;
-    for (int c = cmax; c >= 0; --c)
-      for (int b = bmax; b >= 0; --b)
-        for (int a = amax; a >= 0; --a) {
-          if (a | b | c) {
-            const int64_t nb = el - a - int64_t(b) * sl.Ex - int64_t(c) * sl.Ex * sl.Ey;
-            acc += __ldcg(&dep[nb * NLOC + (k + c * q) * ND2 + (j + b * q) * ND + (i + a * q)]);
-          } else {
-            acc += out[k];
-          }
-        }
-    const int64_t z = zb + k;
-    epi(sl.lidx(x, y, z), sl.masked(x, y, z) ? 0.0 : acc);
+  for (int kb = 0; kb < ND; kb += KH) {
+    double cx[KH], cy[KH], cxy[KH];
+#pragma unroll
+    for (int kk = 0; kk < KH; ++kk) {
+      const int k = kb + kk;
+      const bool own = k < ND && ownx && owny && (k < q || topz);
+      cx[kk] = ldcg_pred(dbase - LX * NLOC + k * ND2 + q, own && hx);
+      cy[kk] = ldcg_pred(dbase - LY * NLOC + k * ND2 + q * ND, own && hy);
+      cxy[kk] = ldcg_pred(dbase - (LX + LY) * NLOC + k * ND2 + q * ND + q, own && hx && hy);
+    }
+#pragma unroll
+    for (int kk = 0; kk < KH; ++kk) {
+      const int k = kb + kk;
+      if (k >= ND || !(ownx && owny && (k < q || topz))) continue;
+      double acc = 0.0;
+      if (k == 0) {  // (c=1): (b,a) = (1,1), (1,0), (0,1), (0,0)
+        acc += cxyz;
+        acc += cyz;
+        acc += cxz;
+        acc += cz;
+      }
+      acc += cxy[kk];  // (c=0): (1,1), (1,0), (0,1), then the element itself
+      acc += cy[kk];
+      acc += cx[kk];
+      acc += out[k];
+      const int64_t z = zb + k;
+      epi(sl.lidx(x, y, z), sl.masked(x, y, z) ? 0.0 : acc);
+    }
   }
 }
 
@@ -340,7 +376,7 @@ int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, cons
   const int64_t nE = sl.elems();
   if (nE == 0) return 0;
   const int ngroups = int((nE + EPB - 1) / EPB);
-  const size_t smem = (size_t(EPB) * 8 * NLOC + ND * ND) * sizeof(double);
+  const size_t smem = (size_t(EPB) * 2 * NLOC + ND * ND) * sizeof(double);
   auto kern = k_ax<ND, EPB, LOCAL, EpiT>;
   static bool configured = false;  // per instantiation
   if (!configured) {

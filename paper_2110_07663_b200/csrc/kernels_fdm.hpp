@@ -25,7 +25,7 @@ int64_t launch_ras(const Slab& sl, int precision, const void* S, const void* L, 
 int64_t launch_asm(const Slab& sl, int precision, const void* S, const void* L, const double* r, void* boxes,
                    double* out, cudaStream_t s);
 // fdm_solve on E padded boxes (FP64 in/out).
-int64_t launch_fdm_boxes(int q, int64_t E, int precision, const void* S, const void* L, const double* in,
+int64_t launch_fdm_boxes(const Slab& sl, int precision, const void* S, const void* L, const double* in,
                          double* out, cudaStream_t s);
 
 }  // namespace sb

@@ -222,7 +222,7 @@ int semlab_schwarz_fdm_solve_all(semlab_schwarz sch, const double* in, double* o
   return guard([&] {
     need(sch, "fdm_solve: smoother");
     semlab_space_s& sp = *sch->space;
-    sp.ctx->count(launch_fdm_boxes(sp.order, sp.E, sch->precision, sch->S.p, sch->L.p, in, out, sp.ctx->stream));
+    sp.ctx->count(launch_fdm_boxes(sp.sl, sch->precision, sch->S.p, sch->L.p, in, out, sp.ctx->stream));
   });
 }
 
