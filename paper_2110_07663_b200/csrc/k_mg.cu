@@ -64,11 +64,14 @@ __global__ void k_pass(const double* __restrict__ in, const Grid3 gin, double* _
       int64_t e = I / qc;
       const int a = int(I - e * qc);
       if (a == 0 && e > 0) {  // shared coarse node: left element (a' = qc), then right element
-        for (int i = 0; i <= qf; ++i) {
-          const double w = J.v[i * jn + qc];
-          if (w != 0.0) acc += w * fetch((e - 1) * qf + i);
-        }
-        if (e < E_axis)
+        // (on a slab, an element of the other rank contributes through the interface sum; the
+        // shared fine node X = e qf is counted with the left element only)
+        if (e - 1 >= J.e_lo)
+          for (int i = 0; i <= qf; ++i) {
+            const double w = J.v[i * jn + qc];
+            if (w != 0.0) acc += w * fetch((e - 1) * qf + i);
+          }
+        if (e < E_axis && e < J.e_hi)
           for (int i = 1; i <= qf; ++i) {
             const double w = J.v[i * jn + 0];
             if (w != 0.0) acc += w * fetch(e * qf + i);

@@ -682,6 +682,9 @@ int64_t launch_mul(double* y, const double* a, const double* x, int64_t n, cudaS
 int64_t launch_sub(double* y, const double* a, const double* b, int64_t n, cudaStream_t s) {
   return foreach(n, s, [=] __device__(int64_t t) { y[t] = a[t] - b[t]; });
 }
+int64_t launch_add_planes(double* y, const double* a, const double* b, int64_t n, cudaStream_t s) {
+  return foreach(n, s, [=] __device__(int64_t t) { y[t] = a[t] + b[t]; });
+}
 int64_t launch_div(double* y, const double* x, double a, int64_t n, cudaStream_t s) {
   return foreach(n, s, [=] __device__(int64_t t) { y[t] = x[t] / a; });
 }

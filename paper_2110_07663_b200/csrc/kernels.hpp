@@ -53,6 +53,7 @@ int64_t launch_axpby(double* y, double a, const double* x, double b, int64_t n, 
 int64_t launch_mul(double* y, const double* a, const double* x, int64_t n, cudaStream_t s);       // y = a .* x
 int64_t launch_sub(double* y, const double* a, const double* b, int64_t n, cudaStream_t s);       // y = a - b
 int64_t launch_div(double* y, const double* x, double a, int64_t n, cudaStream_t s);             // y = x / a
+int64_t launch_add_planes(double* y, const double* a, const double* b, int64_t n, cudaStream_t s);  // y = a + b
 // Chebyshev vector steps for a generic surrogate S (chebyshev.cpp:80-95)
 int64_t launch_cheb_init(double* r, double* d, double theta, int64_t n, cudaStream_t s);  // d = r / theta
 int64_t launch_cheb_step(double* x, double* r, double* d, const double* sad, double c1, double c2,

@@ -28,7 +28,8 @@ struct semlab_ctx_s {
   void allreduce_device(double* d_vals, int K);
   void sync() { SB_CUDA(cudaStreamSynchronize(stream)); }
   // Deterministic dots of K vector pairs over [off, off+len) summed over ranks; host result.
-  void dots(int K, const double* const* a, const double* const* b, int64_t off, int64_t len, double* host_out);
+  void dots(int K, const double* const* a, const double* const* b, int64_t off, int64_t len, double* host_out,
+            bool global = true);
 };
 
 struct semlab_mesh_s {
@@ -49,9 +50,13 @@ struct semlab_space_s {
   sb::Slab sl{};
   int64_t n = 0, E = 0, nloc = 0;
   std::vector<double> coords;  // host lattice coords of the local planes (3 per point)
-  sb::DevBuf<double> geom, massw, mass_diag, inv_diag, dep, scratch_e;
+  sb::DevBuf<double> geom, massw, mass_diag, inv_diag, dep, scratch_e, plane_lo, plane_hi;
   sb::DevBuf<unsigned> flags, ticket;
   bool has_inv_diag = false;
+  bool full = false;  // whole mesh on this rank even under a distributed context (coarse solve)
+  bool distributed() const { return !full && ctx->nranks > 1; }
+  void halo_exchange(double* v);
+  void owner_copy_up(double* v);
 
   void build();
   sb::AxSync sync() const { return {dep.p, flags.p, ticket.p}; }

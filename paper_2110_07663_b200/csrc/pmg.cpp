@@ -2,6 +2,7 @@
 #include "pmg.hpp"
 
 #include <cusolverDn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -26,7 +27,7 @@ double HostCsr::coeff(int64_t i, int64_t j) const {
 // assembled like setFromTriplets (duplicates summed in insertion order: ascending element).
 HostCsr assemble_free_matrix(semlab_space sp) {
   if (sp->bc != SEMLAB_BC_DIRICHLET) invalid("coarse solve: only the Dirichlet problem is supported");
-  if (sp->ctx->nranks > 1) invalid("coarse solve: assemble on a single-rank space");
+  if (sp->distributed()) invalid("coarse solve: assemble on a whole-mesh space");
   const int q = sp->order, nd = q + 1, nl = nd * nd * nd, nd2 = nd * nd;
   const int64_t E = sp->E;
   std::vector<double> geom(size_t(E) * 6 * nl);
@@ -372,6 +373,40 @@ void CoarseSolver::solve(const double* r_full, double* z_full) {
   c->count(launch_scatter_free(sp->sl, zf.p, z_full, s));
 }
 
+// Distributed coarse level: every rank contributes its owned p=1 planes (ncclAllGather of
+// equal-size padded blocks), solves the whole coarse problem redundantly, and keeps its slab.
+void CoarseSolver::solve_dist(semlab_space dsp, const double* r_loc, double* z_loc) {
+  semlab_ctx c = dsp->ctx;
+  cudaStream_t s = c->stream;
+  const Slab& ls = dsp->sl;
+  const int64_t P = ls.Nx * ls.Ny;
+  const int R = c->nranks;
+  int64_t maxpl = 0;
+  std::vector<int64_t> z0(static_cast<size_t>(R)), z1(static_cast<size_t>(R));
+  for (int k = 0; k < R; ++k) {
+    const Slab sk = make_slab(ls.q, ls.Ex, ls.Ey, ls.Ez, k, R, ls.dirichlet != 0);
+    z0[size_t(k)] = sk.own_z0();
+    z1[size_t(k)] = sk.own_z1();
+    maxpl = std::max(maxpl, z1[size_t(k)] - z0[size_t(k)]);
+  }
+  if (gsend.n < size_t(maxpl * P)) {
+    gsend.alloc(size_t(maxpl * P));
+    grecv.alloc(size_t(maxpl * P * R));
+    rfull.alloc(size_t(sp->n));
+    zfull.alloc(size_t(sp->n));
+  }
+  const int me = c->rank;
+  SB_CUDA(cudaMemcpyAsync(gsend.p, r_loc + ls.lidx(0, 0, z0[size_t(me)]),
+                          size_t((z1[size_t(me)] - z0[size_t(me)]) * P) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  ncclResult_t rr = ncclAllGather(gsend.p, grecv.p, size_t(maxpl * P), ncclDouble, static_cast<ncclComm_t>(c->nccl), s);
+  if (rr != ncclSuccess) fail(kNccl, std::string("ncclAllGather: ") + ncclGetErrorString(rr));
+  for (int k = 0; k < R; ++k)
+    SB_CUDA(cudaMemcpyAsync(rfull.p + z0[size_t(k)] * P, grecv.p + size_t(k) * maxpl * P,
+                            size_t((z1[size_t(k)] - z0[size_t(k)]) * P) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  solve(rfull.p, zfull.p);
+  SB_CUDA(cudaMemcpyAsync(z_loc, zfull.p + ls.zlo * P, size_t(ls.nzl * P) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
 }  // namespace sb
 
 // ------------------------------------------------------------------------ hierarchy
@@ -396,6 +431,7 @@ semlab_pmg_s::~semlab_pmg_s() {
     delete L.sch;
     delete L.sp;
   }
+  delete coarse_full;
 }
 
 void semlab_pmg_s::build() {
@@ -404,7 +440,6 @@ void semlab_pmg_s::build() {
   for (size_t l = 0; l + 1 < nl; ++l)
     if (!(orders[l] > orders[l + 1])) invalid("pmg: schedule must be strictly decreasing");
   if (orders.back() != 1) invalid("pmg: schedule must end at order 1");
-  if (ctx->nranks > 1) invalid("pmg: distributed hierarchies are not enabled in this build");
   lv.resize(nl);
   for (size_t l = 0; l < nl; ++l) {
     Level& L = lv[l];
@@ -464,7 +499,19 @@ void semlab_pmg_s::build() {
   }
   tA.alloc(scratch);
   tB.alloc(scratch);
-  coarse.build(lv.back().sp, coarse_mode);
+  if (lv.back().sp->distributed()) {
+    auto full = std::make_unique<semlab_space_s>();
+    full->ctx = ctx;
+    full->mesh = mesh;
+    full->order = orders.back();
+    full->bc = SEMLAB_BC_DIRICHLET;
+    full->full = true;
+    full->build();
+    coarse_full = full.release();
+    coarse.build(coarse_full, coarse_mode);
+  } else {
+    coarse.build(lv.back().sp, coarse_mode);
+  }
   ctx->sync();
 }
 
@@ -504,7 +551,11 @@ void semlab_pmg_s::restrict_(int l, const double* fv, double* cv) {
   const int64_t zbc = int64_t(c.ez0) * qc, nzc = int64_t(c.ez1 - c.ez0) * qc + 1;
   ctx->count(launch_transfer_pass(false, fv, gf, tA.p, g1, 0, J[size_t(l)], qf, qc, f.Ex, true, gf, false, gc, zbf, nzf, s));
   ctx->count(launch_transfer_pass(false, tA.p, g1, tB.p, g2, 1, J[size_t(l)], qf, qc, f.Ey, false, gf, false, gc, zbf, nzf, s));
-  ctx->count(launch_transfer_pass(false, tB.p, g2, cv, gc, 2, J[size_t(l)], qf, qc, f.Ez, false, gf, true, gc, zbc, nzc, s));
+  Jmat Jz = J[size_t(l)];
+  Jz.e_lo = f.ez0;  // z: only this slab's element layers contribute; the other rank's part
+  Jz.e_hi = f.ez1;  // arrives through the interface-plane sum below
+  ctx->count(launch_transfer_pass(false, tB.p, g2, cv, gc, 2, Jz, qf, qc, f.Ez, false, gf, true, gc, zbc, nzc, s));
+  lv[size_t(l) + 1].sp->interface_sum(cv);
 }
 
 // Alg. 1 with x0 = 0: pre-smooth, residual, restrict, recurse, correct, post-smooth.
@@ -512,7 +563,10 @@ void semlab_pmg_s::cycle(int l) {
   Level& L = lv[size_t(l)];
   cudaStream_t s = ctx->stream;
   if (l == int(lv.size()) - 1) {
-    coarse.solve(L.b.p, L.x.p);
+    if (coarse_full)
+      coarse.solve_dist(L.sp, L.b.p, L.x.p);
+    else
+      coarse.solve(L.b.p, L.x.p);
     return;
   }
   const int64_t n = L.sp->n;

@@ -55,8 +55,10 @@ struct CoarseSolver {
   DevBuf<double> coarse_inv;
   int64_t coarse_n = 0;
   double omega = 0.9;
+  DevBuf<double> gsend, grecv, rfull, zfull;  // distributed gather of the coarse residual
   void build(semlab_space space, int mode);
   void solve(const double* r_full, double* z_full);
+  void solve_dist(semlab_space dist_space, const double* r_loc, double* z_loc);
   void amg_cycle(int l, const double* r, double* z);
 };
 
@@ -80,6 +82,7 @@ struct semlab_pmg_s {
   std::vector<sb::Jmat> J;  // J[l]: level l+1 (coarse) -> level l (fine)
   sb::DevBuf<double> tA, tB;  // transfer scratch
   sb::CoarseSolver coarse;
+  semlab_space coarse_full = nullptr;  // whole-mesh p=1 space for the redundant coarse solve
   ~semlab_pmg_s();
   void build();
   void prolong(int l, const double* coarse_v, double* fine_v);

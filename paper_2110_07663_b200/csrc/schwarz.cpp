@@ -178,10 +178,16 @@ void semlab_schwarz_s::apply(const double* r, double* z) {
   if (r == z) invalid("SchwarzSmoother::apply: in and out must not alias");
   semlab_space_s& sp = *space;
   SB_CUDA(cudaMemsetAsync(z, 0, size_t(sp.n) * sizeof(double), sp.ctx->stream));
+  if (sp.distributed()) {
+    if (mode != SEMLAB_SCHWARZ_RAS) invalid("SchwarzSmoother: ASM is not available on a distributed space (use RAS)");
+    // the ghost planes of a slab vector are scratch: fill them with the neighbours' planes
+    sp.halo_exchange(const_cast<double*>(r));
+  }
   if (mode == SEMLAB_SCHWARZ_RAS) {
     RasEpi e;
     e.out = z;
     ras(r, 0, e);
+    sp.owner_copy_up(z);
   } else {
     sp.ctx->count(launch_asm(sp.sl, precision, S.p, L.p, r, boxes.p, z, sp.ctx->stream));
   }

@@ -20,12 +20,12 @@ cudaStream_t st(semlab_ctx c) { return c->stream; }
 // planes need the cross-rank sum before the owner epilogue).
 bool fused_jacobi(semlab_op S, semlab_op A) {
   return S->kind == semlab_op_s::kJacobi && A->kind == semlab_op_s::kA && S->space == A->space &&
-         A->ctx->nranks == 1;
+         !A->space->distributed();
 }
 
 bool fused_ras(semlab_op S, semlab_op A) {
   return S->kind == semlab_op_s::kSchwarz && S->sch->mode == SEMLAB_SCHWARZ_RAS && A->kind == semlab_op_s::kA &&
-         S->space == A->space && A->ctx->nranks == 1;
+         S->space == A->space && !A->space->distributed();
 }
 
 }  // namespace

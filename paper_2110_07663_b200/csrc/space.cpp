@@ -25,7 +25,7 @@ void semlab_ctx_s::allreduce_device(double* d_vals, int K) {
 }
 
 void semlab_ctx_s::dots(int K, const double* const* a, const double* const* b, int64_t off, int64_t len,
-                        double* host_out) {
+                        double* host_out, bool global) {
   const double* aa[4];
   const double* bb[4];
   for (int k = 0; k < K; ++k) {
@@ -33,7 +33,7 @@ void semlab_ctx_s::dots(int K, const double* const* a, const double* const* b, i
     bb[k] = b[k] + off;
   }
   count(launch_dots(K, aa, bb, len, dot_out.p, dots(), stream));
-  allreduce_device(dot_out.p, K);
+  if (global) allreduce_device(dot_out.p, K);
   SB_CUDA(cudaMemcpyAsync(host_pinned, dot_out.p, sizeof(double) * K, cudaMemcpyDeviceToHost, stream));
   sync();
   for (int k = 0; k < K; ++k) host_out[k] = host_pinned[k];
@@ -86,11 +86,11 @@ std::vector<double> semlab_mesh_s::lattice_planes(int order, int64_t z0, int64_t
 // ------------------------------------------------------------------------------ space
 void semlab_space_s::build() {
   if (order < 1 || order > 9) invalid("SemSpace: order must be in [1,9] for the device kernels, got " + std::to_string(order));
-  if (ctx->nranks > mesh->dims[2])
-    invalid("SemSpace: more ranks (" + std::to_string(ctx->nranks) + ") than element layers in z (" +
+  const int rk = full ? 0 : ctx->rank, nr = full ? 1 : ctx->nranks;
+  if (nr > mesh->dims[2])
+    invalid("SemSpace: more ranks (" + std::to_string(nr) + ") than element layers in z (" +
             std::to_string(mesh->dims[2]) + ")");
-  sl = make_slab(order, mesh->dims[0], mesh->dims[1], mesh->dims[2], ctx->rank, ctx->nranks,
-                 bc == SEMLAB_BC_DIRICHLET);
+  sl = make_slab(order, mesh->dims[0], mesh->dims[1], mesh->dims[2], rk, nr, bc == SEMLAB_BC_DIRICHLET);
   const int nd = order + 1;
   nloc = int64_t(nd) * nd * nd;
   E = sl.elems();
@@ -120,9 +120,68 @@ void semlab_space_s::build() {
   ctx->sync();
 }
 
+// ---- slab exchanges over NCCL (grouped send/recv between z-neighbour ranks) ---------------
+// Interface planes z = ez0 q (shared with rank-1) and z = ez1 q (shared with rank+1) hold this
+// rank's partial Q^T sums after a gather-type operation; both ranks add lower + upper partial in
+// that order, so the duplicated planes stay bitwise identical on the two ranks.
 void semlab_space_s::interface_sum(double* v) {
-  if (ctx->nranks <= 1) return;
-  invalid("interface_sum: distributed spaces are not enabled in this build");
+  if (!distributed()) return;
+  const int64_t P = sl.Nx * sl.Ny;
+  if (plane_lo.n < size_t(P)) {
+    plane_lo.alloc(size_t(P));
+    plane_hi.alloc(size_t(P));
+  }
+  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+  cudaStream_t s = ctx->stream;
+  const int r = ctx->rank;
+  double* vb = v + sl.lidx(0, 0, int64_t(sl.ez0) * sl.q);
+  double* vt = v + sl.lidx(0, 0, int64_t(sl.ez1) * sl.q);
+  SB_NCCL(ncclGroupStart());
+  if (sl.nranks_below) {
+    SB_NCCL(ncclSend(vb, size_t(P), ncclDouble, r - 1, comm, s));
+    SB_NCCL(ncclRecv(plane_lo.p, size_t(P), ncclDouble, r - 1, comm, s));
+  }
+  if (sl.nranks_above) {
+    SB_NCCL(ncclSend(vt, size_t(P), ncclDouble, r + 1, comm, s));
+    SB_NCCL(ncclRecv(plane_hi.p, size_t(P), ncclDouble, r + 1, comm, s));
+  }
+  SB_NCCL(ncclGroupEnd());
+  if (sl.nranks_below) ctx->count(launch_add_planes(vb, plane_lo.p, vb, P, s));  // lower partial first
+  if (sl.nranks_above) ctx->count(launch_add_planes(vt, vt, plane_hi.p, P, s));
+}
+
+// Ghost planes z = ez0 q - 1 and z = ez1 q + 1 (the Schwarz halo, schwarz.cpp:159-168).
+void semlab_space_s::halo_exchange(double* v) {
+  if (!distributed()) return;
+  const int64_t P = sl.Nx * sl.Ny;
+  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+  cudaStream_t s = ctx->stream;
+  const int r = ctx->rank;
+  const int64_t zb = int64_t(sl.ez0) * sl.q, zt = int64_t(sl.ez1) * sl.q;
+  SB_NCCL(ncclGroupStart());
+  if (sl.nranks_below) {
+    SB_NCCL(ncclSend(v + sl.lidx(0, 0, zb + 1), size_t(P), ncclDouble, r - 1, comm, s));
+    SB_NCCL(ncclRecv(v + sl.lidx(0, 0, zb - 1), size_t(P), ncclDouble, r - 1, comm, s));
+  }
+  if (sl.nranks_above) {
+    SB_NCCL(ncclSend(v + sl.lidx(0, 0, zt - 1), size_t(P), ncclDouble, r + 1, comm, s));
+    SB_NCCL(ncclRecv(v + sl.lidx(0, 0, zt + 1), size_t(P), ncclDouble, r + 1, comm, s));
+  }
+  SB_NCCL(ncclGroupEnd());
+}
+
+// The interface plane z = ez1 q is owned by the lower rank for owner-write operators (RAS):
+// copy it up so both ranks hold the owner's value.
+void semlab_space_s::owner_copy_up(double* v) {
+  if (!distributed()) return;
+  const int64_t P = sl.Nx * sl.Ny;
+  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+  cudaStream_t s = ctx->stream;
+  const int r = ctx->rank;
+  SB_NCCL(ncclGroupStart());
+  if (sl.nranks_above) SB_NCCL(ncclSend(v + sl.lidx(0, 0, int64_t(sl.ez1) * sl.q), size_t(P), ncclDouble, r + 1, comm, s));
+  if (sl.nranks_below) SB_NCCL(ncclRecv(v + sl.lidx(0, 0, int64_t(sl.ez0) * sl.q), size_t(P), ncclDouble, r - 1, comm, s));
+  SB_NCCL(ncclGroupEnd());
 }
 
 void semlab_space_s::ax(const double* in, Epi epi, const EpiArgs& a) {
@@ -144,7 +203,7 @@ void semlab_space_s::apply_A(const double* in, double* out) {
     const double* av[1] = {out};
     const double* bv[1] = {ones.p};
     double sum = 0.0;
-    ctx->dots(1, av, bv, own_off(), own_len(), &sum);
+    ctx->dots(1, av, bv, own_off(), own_len(), &sum, distributed());
     const double mean = sum / double(sl.Nx * sl.Ny * sl.Nz);
     ctx->count(launch_axpby(out, -mean, ones.p, 1.0, n, ctx->stream));
   }
@@ -175,7 +234,7 @@ double semlab_space_s::dot(const double* a, const double* b) {
   const double* av[1] = {a};
   const double* bv[1] = {b};
   double r = 0.0;
-  ctx->dots(1, av, bv, own_off(), own_len(), &r);
+  ctx->dots(1, av, bv, own_off(), own_len(), &r, distributed());
   return r;
 }
 

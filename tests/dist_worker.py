@@ -1,0 +1,88 @@
+"""Distributed (z-slab, NCCL) parity worker: launched by tests/test_dist_gpu.py through torchrun.
+
+Every rank owns a slab of elements; results are gathered on the owned planes and compared with
+the CPU oracle on the whole mesh. Prints one JSON line of errors / iteration counts on rank 0.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import semlab_np as o  # noqa: E402
+from paper_2110_07663_b200 import semlab as S  # noqa: E402
+from paper_2110_07663_b200.partition import Slab  # noqa: E402
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    uid = [S.Context.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    ctx = S.Context(local, torch.cuda.current_stream(local), rank, world, uid[0])
+    eps, E, p = float(os.environ.get("DIST_EPS", "0.3")), int(os.environ.get("DIST_E", "4")), 7
+    sl = Slab(p, E, E, E, rank, world)
+
+    def gather(vec):
+        """owned planes of every rank -> full global vector (numpy) on every rank"""
+        v = vec.detach().cpu().numpy() if isinstance(vec, torch.Tensor) else vec
+        parts = [None] * world
+        dist.all_gather_object(parts, v[sl.owned_slice_local()])
+        return np.concatenate(parts)
+
+    def rel(a, b):
+        return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+    out = {"world": world}
+    mesh = S.generate_kershaw(eps, E, ctx)
+    sp = S.SemSpace(mesh, p)
+    c = o.SemSpace(o.generate_kershaw(eps, E), p)
+    assert sp.n == sl.n_local, (sp.n, sl.n_local)
+    u = np.random.default_rng(0).standard_normal(c.n)
+    w = sp.apply_A(u[sl.local_slice()])
+    out["ax"] = rel(gather(w), c.apply_A(u))
+    # duplicated interface planes must agree with the global result too
+    wl = w.cpu().numpy()
+    ref = c.apply_A(u)
+    a = (sl.ez0 * p - sl.zlo) * sl.plane
+    b = (sl.ez1 * p - sl.zlo + 1) * sl.plane
+    out["ax_all_planes"] = rel(wl[a:b], ref[sl.ez0 * p * sl.plane:(sl.ez1 * p + 1) * sl.plane])
+    out["dot"] = abs(sp.dot(sp.to_device(u[sl.local_slice()]), w) - float(u @ ref)) / abs(float(u @ ref))
+    out["mass"] = rel(gather(sp.mass_diag()), c.mass_diag)
+    out["diag"] = rel(gather(sp.stiffness_diag()), c.stiffness_diag())
+
+    sch = S.SchwarzSmoother(sp, S.RAS, 64)
+    so = o.SchwarzSmoother(c, o.RAS, 64)
+    r = c.mask_inplace(np.random.default_rng(1).standard_normal(c.n))
+    out["ras64"] = rel(gather(sch.apply(r[sl.local_slice()])), so.apply(r))
+
+    pm = S.Pmg(mesh, (7, 3, 1), S.RAS_SMOOTHER, 2, 0.1, 1.1, 64, S.COARSE_DIRECT)
+    pmo = o.Pmg(o.generate_kershaw(eps, E), (7, 3, 1), "ras", 2, 0.1, 1.1, "direct", 64)
+    out["lam"] = [abs(pm.lam(l) - pmo.levels[l]["lam"]) / pmo.levels[l]["lam"] for l in range(2)]
+    bo = o.build_rhs(c, 1)
+    b_loc = pm.spaces[0].build_rhs(1)
+    out["rhs"] = rel(gather(b_loc), bo)
+    out["vcycle"] = rel(gather(pm.vcycle(b_loc)), pmo.vcycle(bo))
+
+    x = torch.zeros_like(b_loc)
+    st = S.gmres_solve(pm.spaces[0].as_linop(), pm.as_linop(), b_loc, x, S.GmresConfig())
+    xo = np.zeros(c.n)
+    sto = o.gmres_solve(c.apply_A, pmo.vcycle, bo, xo, o.GmresConfig())
+    out["gmres_iters"] = [st.iterations, sto.iterations]
+    out["gmres_conv"] = bool(st.converged)
+    out["gmres_x"] = rel(gather(x), xo)
+    if rank == 0:
+        print("DIST_RESULT " + json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
