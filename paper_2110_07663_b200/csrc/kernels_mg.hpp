@@ -17,7 +17,7 @@ struct Grid3 {
 };
 
 struct Jmat {  // (qf+1) x (qc+1) row-major, qf <= 15
-  double v[16 * 16];
+  double v[16 * 16] = {};
   int e_lo = 0, e_hi = 1 << 30;  // elements along the pass axis present on this rank (restrict)
 };
 

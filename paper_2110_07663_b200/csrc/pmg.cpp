@@ -491,7 +491,7 @@ void semlab_pmg_s::build() {
   for (size_t l = 0; l + 1 < nl; ++l) {
     const int qf = orders[l], qc = orders[l + 1];
     const auto Jv = lagrange_interpolation_matrix(gll(qc).nodes, gll(qf).nodes);
-    std::memset(&J[l], 0, sizeof(Jmat));
+    J[l] = Jmat{};
     for (size_t t = 0; t < Jv.size(); ++t) J[l].v[t] = Jv[t];
     const Slab& f = lv[l].sp->sl;
     const Slab& c = lv[l + 1].sp->sl;
@@ -572,10 +572,15 @@ void semlab_pmg_s::cycle(int l) {
   const int64_t n = L.sp->n;
   SB_CUDA(cudaMemsetAsync(L.x.p, 0, size_t(n) * sizeof(double), s));
   L.cheb->smooth(L.b.p, L.x.p, true);
-  EpiArgs a;
-  a.w = L.r.p;
-  a.b = L.b.p;
-  L.sp->ax(L.x.p, Epi::Residual, a);
+  if (L.sp->distributed()) {  // the residual needs the summed interface planes first
+    L.sp->apply_A(L.x.p, L.r.p);
+    ctx->count(launch_sub(L.r.p, L.b.p, L.r.p, n, s));
+  } else {
+    EpiArgs a;
+    a.w = L.r.p;
+    a.b = L.b.p;
+    L.sp->ax(L.x.p, Epi::Residual, a);
+  }
   restrict_(l, L.r.p, lv[size_t(l) + 1].b.p);
   cycle(l + 1);
   prolong(l, lv[size_t(l) + 1].x.p, L.r.p);

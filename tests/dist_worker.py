@@ -19,6 +19,12 @@ from paper_2110_07663_b200 import semlab as S  # noqa: E402
 from paper_2110_07663_b200.partition import Slab  # noqa: E402
 
 
+def _allg(x, world):
+    parts = [None] * world
+    dist.all_gather_object(parts, x)
+    return parts
+
+
 def main():
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -69,6 +75,24 @@ def main():
     bo = o.build_rhs(c, 1)
     b_loc = pm.spaces[0].build_rhs(1)
     out["rhs"] = rel(gather(b_loc), bo)
+    # transfers (level 0 <-> 1 and 1 <-> 2) on slabs
+    for lvl in range(2):
+        slf, slc = Slab(pm.orders[lvl], E, E, E, rank, world), Slab(pm.orders[lvl + 1], E, E, E, rank, world)
+        T = pmo.transfers[lvl]
+        uc = np.random.default_rng(5 + lvl).standard_normal(pmo.spaces[lvl + 1].n)
+        vf = np.random.default_rng(7 + lvl).standard_normal(pmo.spaces[lvl].n)
+        Pu = pm.prolong(lvl, pm.spaces[lvl + 1].to_device(uc[slc.local_slice()]))
+        PTv = pm.restrict(lvl, pm.spaces[lvl].to_device(vf[slf.local_slice()]))
+        slf_g = lambda v, s=slf: np.concatenate(_allg(v.cpu().numpy()[s.owned_slice_local()], world))
+        slc_g = lambda v, s=slc: np.concatenate(_allg(v.cpu().numpy()[s.owned_slice_local()], world))
+        out[f"prolong{lvl}"] = rel(slf_g(Pu), T.prolong(uc))
+        out[f"restrict{lvl}"] = rel(slc_g(PTv), T.restrict(vf))
+    pmj = S.Pmg(mesh, (3, 1), S.JACOBI_SMOOTHER, 2, 0.1, 1.1, 64, S.COARSE_DIRECT)
+    pmjo = o.Pmg(o.generate_kershaw(eps, E), (3, 1), "jacobi", 2, 0.1, 1.1, "direct", 64)
+    s3 = Slab(3, E, E, E, rank, world)
+    b3 = o.build_rhs(pmjo.spaces[0], 1)
+    z3 = pmj.vcycle(pmj.spaces[0].to_device(b3[s3.local_slice()]))
+    out["vcycle_jac_31"] = rel(np.concatenate(_allg(z3.cpu().numpy()[s3.owned_slice_local()], world)), pmjo.vcycle(b3))
     out["vcycle"] = rel(gather(pm.vcycle(b_loc)), pmo.vcycle(bo))
 
     x = torch.zeros_like(b_loc)

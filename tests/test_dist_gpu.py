@@ -33,7 +33,10 @@ def test_distributed_matches_oracle(nproc):
     assert r["ras64"] < 1e-12
     assert max(r["lam"]) < 1e-9
     assert r["rhs"] < 1e-13
-    assert r["vcycle"] < 1e-10
+    for k in ("prolong0", "prolong1", "restrict0", "restrict1"):
+        assert r[k] < 1e-13, (k, r)
+    assert r["vcycle_jac_31"] < 1e-10, r
+    assert r["vcycle"] < 1e-10, r
     it, ito = r["gmres_iters"]
     assert r["gmres_conv"] and abs(it - ito) <= 1
     assert r["gmres_x"] < 1e-10
