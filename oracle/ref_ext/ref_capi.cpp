@@ -1,0 +1,229 @@
+// ORACLE TEST INFRASTRUCTURE — extern "C" entry points over the reference semlab library (own
+// TUs + Eigen shim) and its restated extension, used by tests/golden/make_golden.py to produce
+// golden vectors and by tests/test_oracle_pin.py to pin the numpy oracle. Output: oracle/_ref/.
+#include <cstring>
+#include <random>
+
+#include "ref_ext.hpp"
+
+using namespace semlab;
+using namespace semlab_ref;
+
+namespace {
+thread_local std::string g_err;
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+HexMesh mesh_of(double eps, int E, int p) { return generate_kershaw(KershawParams{eps, E}, p); }
+std::vector<int> orders_of(const int* o, int n) { return std::vector<int>(o, o + n); }
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_gll(int p, double* nodes, double* weights, double* diff) {
+  return guard([&] {
+    const Gll1D& g = gll(p);
+    std::memcpy(nodes, g.nodes.data(), sizeof(double) * size_t(p + 1));
+    std::memcpy(weights, g.weights.data(), sizeof(double) * size_t(p + 1));
+    std::memcpy(diff, g.diff.data(), sizeof(double) * size_t((p + 1) * (p + 1)));
+  });
+}
+
+int ref_uniform(uint64_t seed, int64_t n, double* out) {
+  return guard([&] {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    for (int64_t i = 0; i < n; ++i) out[i] = dist(rng);
+  });
+}
+
+int ref_sizes(double eps, int E, int p, int64_t* n, int64_t* nlocal) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    *n = s.n();
+    *nlocal = s.n_local_total();
+  });
+}
+
+int ref_lattice(double eps, int E, int p, double* out) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    auto c = m.lattice_coords(p);
+    std::memcpy(out, c.data(), c.size() * sizeof(double));
+  });
+}
+
+int ref_geom(double eps, int E, int p, double* out) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    const int nl = s.nodes_per_element();
+    for (int e = 0; e < m.n_elements(); ++e)
+      for (int node = 0; node < nl; ++node) std::memcpy(out + (size_t(e) * nl + node) * 6, s.metric_at(e, node), 48);
+  });
+}
+
+int ref_apply_A(double eps, int E, int p, const double* u, double* out) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    FieldVector v = Eigen::Map<const Eigen::MatrixXd>(u, s.n(), 1);
+    FieldVector w = s.apply_A(v);
+    std::memcpy(out, w.data(), sizeof(double) * size_t(s.n()));
+  });
+}
+
+int ref_diag_mass(double eps, int E, int p, double* diag, double* mass) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    FieldVector d = s.stiffness_diag();
+    std::memcpy(diag, d.data(), sizeof(double) * size_t(s.n()));
+    std::memcpy(mass, s.mass_diag().data(), sizeof(double) * size_t(s.n()));
+  });
+}
+
+int ref_gather(double eps, int E, int p, const double* loc, double* out) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    FieldVector l = Eigen::Map<const Eigen::MatrixXd>(loc, s.n_local_total(), 1);
+    FieldVector g = s.gather(l);
+    std::memcpy(out, g.data(), sizeof(double) * size_t(s.n()));
+  });
+}
+
+int ref_schwarz_apply(double eps, int E, int p, int mode, const double* r, double* z, double* lengths,
+                      double* lambda0) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    SchwarzSmoother sch(s, mode == 1 ? SchwarzMode::Ras : SchwarzMode::Asm);
+    FieldVector rv = Eigen::Map<const Eigen::MatrixXd>(r, s.n(), 1);
+    FieldVector zv = sch.apply(rv);
+    std::memcpy(z, zv.data(), sizeof(double) * size_t(s.n()));
+    for (int e = 0; e < m.n_elements(); ++e) {
+      const auto L = sch.box_lengths(e);
+      for (int d = 0; d < 3; ++d) lengths[e * 3 + d] = L[size_t(d)];
+    }
+    const auto& d0 = sch.direction(0, 0);
+    for (Index i = 0; i < d0.lambda.size(); ++i) lambda0[i] = d0.lambda[i];
+  });
+}
+
+int ref_lambda(double eps, int E, int p, int smoother, double* value, int* rounds) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    LinOp A = [&s](const FieldVector& in, FieldVector& out) { out = s.apply_A(in); };
+    LinOp S;
+    std::unique_ptr<SchwarzSmoother> sch;
+    FieldVector inv;
+    if (smoother == 0) {
+      inv = jacobi_inverse_diag(s);
+      S = [&inv](const FieldVector& in, FieldVector& out) { out = inv.cwiseProduct(in); };
+    } else {
+      sch = std::make_unique<SchwarzSmoother>(s, smoother == 1 ? SchwarzMode::Ras : SchwarzMode::Asm);
+      S = sch->as_linop();
+    }
+    const LambdaEstimate est = estimate_lambda_max(S, A, s.n(), 10, 0);
+    *value = est.value;
+    *rounds = est.rounds_used;
+  });
+}
+
+int ref_build_rhs(double eps, int E, int p, uint64_t seed, double* out) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    FieldVector b = build_rhs(s, seed);
+    std::memcpy(out, b.data(), sizeof(double) * size_t(s.n()));
+  });
+}
+
+int ref_cheby_smooth(double eps, int E, int p, int smoother, int eta, double lam, const double* b, double* x) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    LinOp A = [&s](const FieldVector& in, FieldVector& out) { out = s.apply_A(in); };
+    FieldVector inv = jacobi_inverse_diag(s);
+    std::unique_ptr<SchwarzSmoother> sch;
+    LinOp S = [&inv](const FieldVector& in, FieldVector& out) { out = inv.cwiseProduct(in); };
+    if (smoother != 0) {
+      sch = std::make_unique<SchwarzSmoother>(s, smoother == 1 ? SchwarzMode::Ras : SchwarzMode::Asm);
+      S = sch->as_linop();
+    }
+    ChebyshevSmoother cheb(S, A, ChebyParams{eta, 0.1, 1.1, lam});
+    FieldVector bv = Eigen::Map<const Eigen::MatrixXd>(b, s.n(), 1);
+    FieldVector xv = Eigen::Map<const Eigen::MatrixXd>(x, s.n(), 1);
+    cheb.smooth(bv, xv);
+    std::memcpy(x, xv.data(), sizeof(double) * size_t(s.n()));
+  });
+}
+
+int ref_vcycle(double eps, int E, const int* orders, int nlev, const char* smoother, const char* coarse, int eta,
+               const double* b, double* z, double* lams) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, orders[0]);
+    Pmg pmg(m, orders_of(orders, nlev), smoother, eta, 0.1, 1.1, coarse);
+    const Index n = pmg.spaces[0]->n();
+    FieldVector bv = Eigen::Map<const Eigen::MatrixXd>(b, n, 1);
+    FieldVector zv = pmg.vcycle(bv);
+    std::memcpy(z, zv.data(), sizeof(double) * size_t(n));
+    for (size_t l = 0; l < pmg.levels.size(); ++l) lams[l] = pmg.levels[l].lam;
+  });
+}
+
+// Full solve from x0 = 0 with b = build_rhs(seed 1): krylov 0 = GMRES(20), 1 = PCG; precond "none",
+// "jacobi" or a pMG smoother name with the given schedule.
+int ref_solve(double eps, int E, const int* orders, int nlev, const char* precond, const char* coarse, int eta,
+              int krylov, double tol, double* x, int* iters, double* rel_res, double* history, int hcap) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, orders[0]);
+    std::unique_ptr<Pmg> pmg;
+    std::unique_ptr<SemSpace> sp;
+    const SemSpace* s0;
+    LinOp M;
+    FieldVector inv;
+    const std::string pc(precond);
+    if (pc == "none" || (pc == "jacobi" && nlev == 1)) {  // plain (Jacobi-)preconditioned Krylov
+      sp = std::make_unique<SemSpace>(m, orders[0]);
+      s0 = sp.get();
+      if (pc == "jacobi") {
+        inv = jacobi_inverse_diag(*s0);
+        M = [&inv](const FieldVector& in, FieldVector& out) { out = inv.cwiseProduct(in); };
+      }
+    } else {
+      pmg = std::make_unique<Pmg>(m, orders_of(orders, nlev), pc, eta, 0.1, 1.1, coarse);
+      s0 = pmg->spaces[0].get();
+      M = pmg->as_linop();
+    }
+    LinOp A = [s0](const FieldVector& in, FieldVector& out) { out = s0->apply_A(in); };
+    FieldVector b = build_rhs(*s0, 1);
+    FieldVector xv = FieldVector::Zero(s0->n());
+    GmresStats st;
+    if (krylov == 0) {
+      GmresConfig cfg;
+      cfg.tol = tol;
+      st = gmres_solve(A, M, b, xv, cfg);
+    } else {
+      st = pcg_solve(A, M, b, xv, tol, 500);
+    }
+    std::memcpy(x, xv.data(), sizeof(double) * size_t(s0->n()));
+    *iters = st.iterations;
+    *rel_res = st.rel_residual;
+    for (int i = 0; i < hcap && i < int(st.history.size()); ++i) history[i] = st.history[size_t(i)];
+  });
+}
+
+}  // extern "C"
