@@ -275,46 +275,57 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_ras(const Slab 
   const int64_t nE = sl.elems();
   const int64_t e_first = int64_t(blockIdx.x) * EPC;
   fdm_block<P, T, false>(sl, S, L, r, e_first, nE, smem, bx);
-  // owner write by rows of owned sites (all vector loads of a row issued together)
-  constexpr int Q = P - 3;  // order: at most Q owned sites per direction
-  for (int rr = threadIdx.x; rr < EPC * Q * Q; rr += Sh::NT) {
-    const int e = rr / (Q * Q), w = rr % (Q * Q);
-    if (e_first + e >= nE) continue;
-    const Box1D &X = bx[e][0], &Y = bx[e][1], &Z = bx[e][2];
-    const int wa = X.own_hi - X.own_lo + 1, wb = Y.own_hi - Y.own_lo + 1, wc = Z.own_hi - Z.own_lo + 1;
-    if (w >= wb * wc) continue;
-    const int b = Y.own_lo + w % wb, c = Z.own_lo + w / wb;
-    const int64_t g0 = sl.lidx(X.lo + X.own_lo, Y.lo + b, Z.lo + c);
-    const T* zrow = smem + e * SPE + P3 + c * P2 + b * P + X.own_lo;
+  // owner write: sites flattened with a (x) fastest so a warp's accesses are contiguous runs;
+  // U sites per thread per round with every vector load issued before any use
+  constexpr int Q = P - 3, Q3 = Q * Q * Q, U = 4;  // at most Q owned sites per direction
+  for (int base = threadIdx.x; base < EPC * Q3; base += Sh::NT * U) {
+    int64_t g[U];
+    bool ok[U];
+    double z[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = base + u * Sh::NT;
+      const int e = t / Q3, w = t % Q3;
+      const int a = w % Q, b = (w / Q) % Q, c = w / (Q * Q);
+      ok[u] = false;
+      g[u] = 0;  // a valid address for the unconditional loads below
+      z[u] = 0.0;
+      if (t < EPC * Q3 && e_first + e < nE) {
+        const Box1D &X = bx[e][0], &Y = bx[e][1], &Z = bx[e][2];
+        if (a <= X.own_hi - X.own_lo && b <= Y.own_hi - Y.own_lo && c <= Z.own_hi - Z.own_lo) {
+          const int aa = X.own_lo + a, bb = Y.own_lo + b, cc = Z.own_lo + c;
+          ok[u] = true;
+          g[u] = sl.lidx(X.lo + aa, Y.lo + bb, Z.lo + cc);
+          z[u] = double(smem[e * SPE + P3 + cc * P2 + bb * P + aa]);
+        }
+      }
+    }
     if (MODE == 0) {
 #pragma unroll
-      for (int a = 0; a < Q; ++a)
-        if (a < wa) epi.out[g0 + a] = double(zrow[a]);
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) epi.out[g[u]] = z[u];
     } else if (MODE == 1) {  // Chebyshev init: r = S t, d = r / theta  (chebyshev.cpp:82-84)
 #pragma unroll
-      for (int a = 0; a < Q; ++a)
-        if (a < wa) {
-          const double z = double(zrow[a]);
-          epi.r[g0 + a] = z;
-          epi.d[g0 + a] = z / epi.c1;
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) {
+          epi.r[g[u]] = z[u];
+          epi.d[g[u]] = z[u] / epi.c1;
         }
     } else {  // Chebyshev step: x += d; r -= S A d; d = c1 d + c2 r  (chebyshev.cpp:86-92)
-      double dv[Q], rv[Q], xv[Q];
+      double dv[U], rv[U], xv[U];
 #pragma unroll
-      for (int a = 0; a < Q; ++a) {
-        const int64_t ga = g0 + (a < wa ? a : 0);  // clamped: loads are unconditional
-        dv[a] = epi.d[ga];
-        rv[a] = epi.r[ga];
-        xv[a] = epi.x[ga];
+      for (int u = 0; u < U; ++u) {
+        dv[u] = epi.d[g[u]];
+        rv[u] = epi.r[g[u]];
+        xv[u] = epi.x[g[u]];
       }
 #pragma unroll
-      for (int a = 0; a < Q; ++a)
-        if (a < wa) {
-          const double z = double(zrow[a]);
-          epi.x[g0 + a] = xv[a] + dv[a];
-          const double rg = rv[a] - z;
-          epi.r[g0 + a] = rg;
-          epi.d[g0 + a] = epi.c1 * dv[a] + epi.c2 * rg;
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) {
+          epi.x[g[u]] = xv[u] + dv[u];
+          const double rg = rv[u] - z[u];
+          epi.r[g[u]] = rg;
+          epi.d[g[u]] = epi.c1 * dv[u] + epi.c2 * rg;
         }
     }
   }

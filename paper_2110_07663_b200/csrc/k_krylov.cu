@@ -1,7 +1,8 @@
 // Krylov kernels for sm_100a: fused classical Gram-Schmidt passes over the column-major basis
 // V (krylov.cpp:67-72, chebyshev.cpp:36-41), and the basis combination V*y (krylov.cpp:111).
-// Every reduction is deterministic: per-block partials in a fixed shape, then the last block
-// to finish sums the partials in block order.
+// Every reduction is deterministic: per-block partials in a fixed shape, then the last block to
+// finish sums the partials in block order. Kernels are instantiated per column-count bucket
+// (NC >= ncol) so accumulators stay in registers.
 #include <algorithm>
 
 #include "device.cuh"
@@ -18,14 +19,17 @@ struct Coef {
   double c[kMaxCol];
 };
 
-// Sum the per-block partial vectors (ncol each) in block order; last block writes out.
-__device__ __forceinline__ void finish_partials(double (&acc)[kMaxCol], int ncol, double* partial, unsigned* counter,
+// Sum per-block partial vectors (ncol each) in block order; the last block writes out.
+template <int NC>
+__device__ __forceinline__ void finish_partials(double (&acc)[NC], int ncol, double* partial, unsigned* counter,
                                                 double* out) {
-  __shared__ double sred[kMaxCol * (kNT / 32)];
+  __shared__ double sred[NC * (kNT / 32)];
   __shared__ bool last;
-  block_sum<kMaxCol, kNT>(acc, sred);
+  block_sum<NC, kNT>(acc, sred);
   if (threadIdx.x == 0) {
-    for (int c = 0; c < ncol; ++c) partial[blockIdx.x * kMaxCol + c] = acc[c];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)  // static indices keep acc in registers
+      if (c < ncol) partial[blockIdx.x * kMaxCol + c] = acc[c];
     __threadfence();
     last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
@@ -40,82 +44,81 @@ __device__ __forceinline__ void finish_partials(double (&acc)[kMaxCol], int ncol
 }
 
 // h = V^T w over the owned range
+template <int NC>
 __global__ void __launch_bounds__(kNT) k_gemv_t(const double* __restrict__ V, int64_t ldv, int ncol,
                                                 const double* __restrict__ w, int64_t off, int64_t len,
                                                 double* __restrict__ h, double* partial, unsigned* counter) {
-  double acc[kMaxCol];
+  double acc[NC];
 #pragma unroll
-  for (int c = 0; c < kMaxCol; ++c) acc[c] = 0.0;
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
   for (int64_t t = int64_t(blockIdx.x) * kNT + threadIdx.x; t < len; t += int64_t(gridDim.x) * kNT) {
     const int64_t i = off + t;
     const double wi = w[i];
 #pragma unroll
-    for (int c = 0; c < kMaxCol; ++c)
-      if (c < ncol) acc[c] = fma(V[c * ldv + i], wi, acc[c]);
+    for (int c = 0; c < NC; ++c)
+      if (c < ncol) acc[c] = fma(__ldcs(V + c * ldv + i), wi, acc[c]);
   }
-  finish_partials(acc, ncol, partial, counter, h);
+  finish_partials<NC>(acc, ncol, partial, counter, h);
 }
 
 // w -= V h over [0,n); h2 = V^T w over the owned range (one read of V for both)
+template <int NC>
 __global__ void __launch_bounds__(kNT) k_cgs_update_dot(const double* __restrict__ V, int64_t ldv, int ncol,
                                                         double* __restrict__ w, const double* __restrict__ h,
                                                         int64_t n, int64_t off, int64_t len,
                                                         double* __restrict__ h2, double* partial,
                                                         unsigned* counter) {
-  __shared__ double sh[kMaxCol];
-  if (threadIdx.x < kMaxCol) sh[threadIdx.x] = threadIdx.x < ncol ? h[threadIdx.x] : 0.0;
+  __shared__ double sh[NC];
+  if (threadIdx.x < NC) sh[threadIdx.x] = threadIdx.x < ncol ? h[threadIdx.x] : 0.0;
   __syncthreads();
-  double acc[kMaxCol];
+  double acc[NC];
 #pragma unroll
-  for (int c = 0; c < kMaxCol; ++c) acc[c] = 0.0;
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * kNT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kNT) {
-    double v[kMaxCol];
+    double v[NC];
     double wi = w[i];
 #pragma unroll
-    for (int c = 0; c < kMaxCol; ++c)
-      if (c < ncol) {
-        v[c] = V[c * ldv + i];
-        wi -= v[c] * sh[c];
-      }
-    w[i] = wi;
-    if (i >= off && i < off + len) {
-#pragma unroll
-      for (int c = 0; c < kMaxCol; ++c)
-        if (c < ncol) acc[c] = fma(v[c], wi, acc[c]);
+    for (int c = 0; c < NC; ++c) {
+      v[c] = c < ncol ? __ldcs(V + c * ldv + i) : 0.0;
+      wi -= v[c] * sh[c];
     }
+    w[i] = wi;
+    const double wo = (i >= off && i < off + len) ? wi : 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = fma(v[c], wo, acc[c]);
   }
-  finish_partials(acc, ncol, partial, counter, h2);
+  finish_partials<NC>(acc, ncol, partial, counter, h2);
 }
 
 // w -= V h2 over [0,n); nrm2 = w.w over the owned range
+template <int NC>
 __global__ void __launch_bounds__(kNT) k_cgs_update_norm(const double* __restrict__ V, int64_t ldv, int ncol,
                                                          double* __restrict__ w, const double* __restrict__ h2,
                                                          int64_t n, int64_t off, int64_t len,
                                                          double* __restrict__ nrm2, double* partial,
                                                          unsigned* counter) {
-  __shared__ double sh[kMaxCol];
-  if (threadIdx.x < kMaxCol) sh[threadIdx.x] = threadIdx.x < ncol ? h2[threadIdx.x] : 0.0;
+  __shared__ double sh[NC];
+  if (threadIdx.x < NC) sh[threadIdx.x] = threadIdx.x < ncol ? h2[threadIdx.x] : 0.0;
   __syncthreads();
-  double acc[kMaxCol];
-#pragma unroll
-  for (int c = 0; c < kMaxCol; ++c) acc[c] = 0.0;
+  double acc[1] = {0.0};
   for (int64_t i = int64_t(blockIdx.x) * kNT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kNT) {
     double wi = w[i];
 #pragma unroll
-    for (int c = 0; c < kMaxCol; ++c)
-      if (c < ncol) wi -= V[c * ldv + i] * sh[c];
+    for (int c = 0; c < NC; ++c)
+      if (c < ncol) wi -= __ldcs(V + c * ldv + i) * sh[c];
     w[i] = wi;
     if (i >= off && i < off + len) acc[0] = fma(wi, wi, acc[0]);
   }
-  finish_partials(acc, 1, partial, counter, nrm2);
+  finish_partials<1>(acc, 1, partial, counter, nrm2);
 }
 
+template <int NC>
 __global__ void __launch_bounds__(kNT) k_gemv_n(const double* __restrict__ V, int64_t ldv, int ncol, const Coef cf,
                                                 double* __restrict__ y, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * kNT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kNT) {
     double s = 0.0;
 #pragma unroll
-    for (int c = 0; c < kMaxCol; ++c)
+    for (int c = 0; c < NC; ++c)
       if (c < ncol) s += V[c * ldv + i] * cf.c[c];
     y[i] = s;
   }
@@ -127,12 +130,32 @@ void check_ncol(int ncol) {
   if (ncol < 1 || ncol > kMaxCol) invalid("krylov: basis width must be in [1,32], got " + std::to_string(ncol));
 }
 
+// smallest instantiated bucket >= ncol
+#define SB_NC_DISPATCH(ncol, CALL) \
+  do {                             \
+    if ((ncol) <= 4) {             \
+      CALL(4);                     \
+    } else if ((ncol) <= 8) {      \
+      CALL(8);                     \
+    } else if ((ncol) <= 12) {     \
+      CALL(12);                    \
+    } else if ((ncol) <= 16) {     \
+      CALL(16);                    \
+    } else if ((ncol) <= 24) {     \
+      CALL(24);                    \
+    } else {                       \
+      CALL(32);                    \
+    }                              \
+  } while (0)
+
 }  // namespace
 
 int64_t launch_gemv_t(const double* V, int64_t ldv, int ncol, const double* w, int64_t off, int64_t len,
                       double* d_h, const DotScratch& ws, cudaStream_t s) {
   check_ncol(ncol);
-  k_gemv_t<<<blocks_for(len), kNT, 0, s>>>(V, ldv, ncol, w, off, len, d_h, ws.partial, ws.counter);
+#define L_(NC) k_gemv_t<NC><<<blocks_for(len), kNT, 0, s>>>(V, ldv, ncol, w, off, len, d_h, ws.partial, ws.counter)
+  SB_NC_DISPATCH(ncol, L_);
+#undef L_
   SB_LAUNCH_CHECK();
   return 1;
 }
@@ -140,7 +163,10 @@ int64_t launch_gemv_t(const double* V, int64_t ldv, int ncol, const double* w, i
 int64_t launch_cgs_update_dot(const double* V, int64_t ldv, int ncol, double* w, const double* d_h, int64_t n,
                               int64_t off, int64_t len, double* d_h2, const DotScratch& ws, cudaStream_t s) {
   check_ncol(ncol);
-  k_cgs_update_dot<<<blocks_for(n), kNT, 0, s>>>(V, ldv, ncol, w, d_h, n, off, len, d_h2, ws.partial, ws.counter);
+#define L_(NC) \
+  k_cgs_update_dot<NC><<<blocks_for(n), kNT, 0, s>>>(V, ldv, ncol, w, d_h, n, off, len, d_h2, ws.partial, ws.counter)
+  SB_NC_DISPATCH(ncol, L_);
+#undef L_
   SB_LAUNCH_CHECK();
   return 1;
 }
@@ -148,8 +174,11 @@ int64_t launch_cgs_update_dot(const double* V, int64_t ldv, int ncol, double* w,
 int64_t launch_cgs_update_norm(const double* V, int64_t ldv, int ncol, double* w, const double* d_h2, int64_t n,
                                int64_t off, int64_t len, double* d_nrm2, const DotScratch& ws, cudaStream_t s) {
   check_ncol(ncol);
-  k_cgs_update_norm<<<blocks_for(n), kNT, 0, s>>>(V, ldv, ncol, w, d_h2, n, off, len, d_nrm2, ws.partial,
-                                                  ws.counter);
+#define L_(NC)                                                                                                    \
+  k_cgs_update_norm<NC><<<blocks_for(n), kNT, 0, s>>>(V, ldv, ncol, w, d_h2, n, off, len, d_nrm2, ws.partial, \
+                                                      ws.counter)
+  SB_NC_DISPATCH(ncol, L_);
+#undef L_
   SB_LAUNCH_CHECK();
   return 1;
 }
@@ -159,7 +188,9 @@ int64_t launch_gemv_n(const double* V, int64_t ldv, int ncol, const double* c_ho
   check_ncol(ncol);
   Coef cf;
   for (int c = 0; c < kMaxCol; ++c) cf.c[c] = c < ncol ? c_host[c] : 0.0;
-  k_gemv_n<<<blocks_for(n), kNT, 0, s>>>(V, ldv, ncol, cf, y, n);
+#define L_(NC) k_gemv_n<NC><<<blocks_for(n), kNT, 0, s>>>(V, ldv, ncol, cf, y, n)
+  SB_NC_DISPATCH(ncol, L_);
+#undef L_
   SB_LAUNCH_CHECK();
   return 1;
 }

@@ -217,6 +217,34 @@ int64_t launch_amg_restrict(const CsrDev& A, const int64_t* aptr, const int* ame
   return 1;
 }
 
+// res = r - A z (row parallel), then rc[I] = sum of res over aggregate I's members, ascending
+__global__ void k_amg_residual(const int64_t* __restrict__ ptr, const int* __restrict__ idx,
+                               const double* __restrict__ val, const double* __restrict__ r,
+                               const double* __restrict__ z, double* __restrict__ res, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double az = 0.0;
+    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) az += val[k] * z[idx[k]];
+    res[i] = r[i] - az;
+  }
+}
+__global__ void k_amg_aggsum(const int64_t* __restrict__ aptr, const int* __restrict__ amem,
+                             const double* __restrict__ res, double* __restrict__ rc, int64_t nc) {
+  for (int64_t I = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; I < nc; I += int64_t(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t m = aptr[I]; m < aptr[I + 1]; ++m) acc += res[amem[m]];
+    rc[I] = acc;
+  }
+}
+
+int64_t launch_amg_restrict_split(const CsrDev& A, const int64_t* aptr, const int* amem, int64_t nc, const double* r,
+                                  const double* z, double* res, double* rc, cudaStream_t s) {
+  if (A.n <= 0) return 0;
+  k_amg_residual<<<grid_for(A.n), 256, 0, s>>>(A.ptr, A.idx, A.val, r, z, res, A.n);
+  k_amg_aggsum<<<grid_for(nc), 128, 0, s>>>(aptr, amem, res, rc, nc);
+  SB_LAUNCH_CHECK();
+  return 2;
+}
+
 // z += P zc   (amg.cpp:156)
 int64_t launch_amg_prolong(const int* agg, const double* zc, double* z, int64_t n, cudaStream_t s) {
   auto body = [=] __device__(int64_t i) { z[i] += zc[agg[i]]; };

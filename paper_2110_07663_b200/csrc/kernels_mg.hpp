@@ -46,6 +46,8 @@ int64_t launch_amg_relax(const CsrDev& A, const double* inv_diag, double omega, 
                          double* zout, cudaStream_t s);
 int64_t launch_amg_restrict(const CsrDev& A, const int64_t* aptr, const int* amem, int64_t nc, const double* r,
                             const double* z, double* rc, cudaStream_t s);
+int64_t launch_amg_restrict_split(const CsrDev& A, const int64_t* aptr, const int* amem, int64_t nc, const double* r,
+                                  const double* z, double* res, double* rc, cudaStream_t s);
 int64_t launch_amg_prolong(const int* agg, const double* zc, double* z, int64_t n, cudaStream_t s);
 
 }  // namespace sb

@@ -355,7 +355,7 @@ void CoarseSolver::amg_cycle(int l, const double* r, double* z) {
   const CsrDev A{L.n, L.ptr.p, L.idx.p, L.val.p};
   c->count(launch_amg_jacobi0(L.inv_diag.p, omega, r, z, L.n, s));
   Lev& N = lev[size_t(l) + 1];
-  c->count(launch_amg_restrict(A, L.aptr.p, L.amem.p, L.nc, r, z, N.r.p, s));
+  c->count(launch_amg_restrict_split(A, L.aptr.p, L.amem.p, L.nc, r, z, L.t.p, N.r.p, s));
   amg_cycle(l + 1, N.r.p, N.z.p);
   c->count(launch_amg_prolong(L.agg.p, N.z.p, z, L.n, s));
   c->count(launch_amg_relax(A, L.inv_diag.p, omega, r, z, L.t.p, s));

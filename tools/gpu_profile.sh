@@ -6,9 +6,9 @@ python bench.py --steps 2 --warmup 3 > gpurun_out/bench.log 2>&1 || exit 1
 tail -1 gpurun_out/bench.log
 if [ "${NCU:-1}" = "1" ]; then
   python tools/perf_probe.py --E 32 --solve 0 > gpurun_out/probe_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:'k_ax|k_ras' -s 6 -c 4 \
+  ncu --set full --clock-control none --import-source on -k regex:'k_ax|k_ras' -s 6 -c 2 \
       -o gpurun_out/prof_ax_ras -f python tools/perf_probe.py --E 32 --solve 0 > gpurun_out/ncu_full.log 2>&1
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
+  ncu --metrics gpu__time_duration.sum --clock-control none -s 2500 -c 3000 --csv \
       --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 fi
 exit 0
