@@ -146,6 +146,15 @@ __global__ void k_geom(const Slab sl, const DMat<ND> Dm, const W1<ND> w1, const 
 }
 
 // ------------------------------------------------------------------------ Ax
+// SEMLAB_AX_PERSISTENT=0 selects the one-CTA-per-element kernel (kept for A/B measurement).
+bool ax_persistent() {
+  static const bool on = [] {
+    const char* e = std::getenv("SEMLAB_AX_PERSISTENT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int ND>
 constexpr int ax_min_blocks() {  // occupancy target: caps registers so ~20 warps/SM stay resident
   return ND >= 8 ? 10 : 4;
@@ -368,9 +377,249 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
   }
 }
 
+// ------------------------------------------------------------------------ persistent Ax
+// Same arithmetic and summation order as k_ax, restructured so no CTA idles on a neighbour:
+// a resident CTA loops over dynamic tickets; for ticket t it computes the element, deposits
+// the non-owned nodes, writes the owned nodes that have no lower contributor (the 6^3 interior
+// of a p=7 element) right away and publishes its counter; only then does it finish ticket t-1's
+// owned face nodes, whose lower neighbours have long been published. The next ticket is taken,
+// and its geometry prefetched to L2, before the current element is computed.
+template <int ND, class EpiT>
+__global__ void __launch_bounds__(ND* ND, 8)
+    k_axp(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const double* __restrict__ geom,
+          double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int total_tickets,
+          const EpiT epi) {
+  constexpr int ND2 = ND * ND, NLOC = ND2 * ND, NT = ND2;
+  constexpr int q = ND - 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* s_a = reinterpret_cast<double*>(smem_raw);
+  double* s_b = s_a + NLOC;
+  double* s_D = s_b + NLOC;
+  double* s_out[2] = {s_D + ND2, s_D + ND2 + NLOC};  // per-element results awaiting completion
+  __shared__ int s_tk[2];
+  __shared__ unsigned s_epoch;
+  const int tid = threadIdx.x;
+  const int ij = tid, i = ij % ND, j = ij / ND;
+  const int64_t nE = sl.elems();
+  const int64_t LX = 1, LY = sl.Ex, LZ = int64_t(sl.Ex) * sl.Ey;
+  for (int t = tid; t < ND2; t += NT) s_D[t] = Dm.d[t];
+  if (tid == 0) {
+    const int t0 = int(atomicAdd(ticket, 1u));
+    if (t0 == total_tickets - 1) atomicExch(ticket, 0u);
+    s_tk[0] = t0;
+    if (t0 < nE) s_epoch = *reinterpret_cast<volatile unsigned*>(&flags[t0]);
+  }
+  __syncthreads();
+  const unsigned target = s_epoch + 1u;  // every element's counter equals s_epoch at launch
+  int64_t prev = -1;
+  int buf = 0;
+
+  auto coords = [&](int64_t el, int& ex, int& ey, int& ez) {
+    ex = int(el % sl.Ex);
+    ey = int((el / sl.Ex) % sl.Ey);
+    ez = sl.ez0 + int(el / LZ);
+  };
+  // owned node (i,j,k) of element (ex,ey,ez) has no contributor below it
+  auto finish_prev = [&](int64_t pe, const double* pout) {
+    int ex, ey, ez;
+    coords(pe, ex, ey, ez);
+    if (tid < 7) {  // wait for the <= 7 lower neighbours of pe (released long ago, normally)
+      const int a = (tid + 1) & 1, b = ((tid + 1) >> 1) & 1, c = ((tid + 1) >> 2) & 1;
+      if ((!a || ex > 0) && (!b || ey > 0) && (!c || ez > sl.ez0)) {
+        const int64_t nb = pe - a * LX - b * LY - c * LZ;
+        while (ld_relaxed(&flags[nb]) < target) {
+        }
+      }
+    }
+    __syncthreads();
+    const bool hx = (i == 0 && ex > 0), hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
+    const bool ownx = (i < q) || (ex == sl.Ex - 1), owny = (j < q) || (ey == sl.Ey - 1);
+    const bool topz = (ez == sl.ez1 - 1);
+    const int64_t x = int64_t(ex) * q + i, y = int64_t(ey) * q + j, zb = int64_t(ez) * q;
+    const double* dbase = dep + pe * NLOC + ij;
+    const bool own0 = ownx && owny && hz;
+    const double cz = ldcg_pred(dbase - LZ * NLOC + q * ND2, own0);
+    const double cxz = ldcg_pred(dbase - (LZ + LX) * NLOC + q * ND2 + q, own0 && hx);
+    const double cyz = ldcg_pred(dbase - (LZ + LY) * NLOC + q * ND2 + q * ND, own0 && hy);
+    const double cxyz = ldcg_pred(dbase - (LZ + LY + LX) * NLOC + q * ND2 + q * ND + q, own0 && hx && hy);
+    constexpr int KH = (ND + 1) / 2;
+#pragma unroll
+    for (int kb = 0; kb < ND; kb += KH) {
+      double cx[KH], cy[KH], cxy[KH];
+#pragma unroll
+      for (int kk = 0; kk < KH; ++kk) {
+        const int k = kb + kk;
+        const bool own = k < ND && ownx && owny && (k < q || topz);
+        cx[kk] = ldcg_pred(dbase - LX * NLOC + k * ND2 + q, own && hx);
+        cy[kk] = ldcg_pred(dbase - LY * NLOC + k * ND2 + q * ND, own && hy);
+        cxy[kk] = ldcg_pred(dbase - (LX + LY) * NLOC + k * ND2 + q * ND + q, own && hx && hy);
+      }
+#pragma unroll
+      for (int kk = 0; kk < KH; ++kk) {
+        const int k = kb + kk;
+        if (k >= ND || !(ownx && owny && (k < q || topz))) continue;
+        if (!(hx || hy || (k == 0 && hz))) continue;  // interior-owned: already written
+        double acc = 0.0;
+        if (k == 0) {  // (c=1): (b,a) = (1,1), (1,0), (0,1), (0,0)
+          acc += cxyz;
+          acc += cyz;
+          acc += cxz;
+          acc += cz;
+        }
+        acc += cxy[kk];  // (c=0): (1,1), (1,0), (0,1), then the element itself
+        acc += cy[kk];
+        acc += cx[kk];
+        acc += pout[k * ND2 + ij];
+        const int64_t z = zb + k;
+        epi(sl.lidx(x, y, z), sl.masked(x, y, z) ? 0.0 : acc);
+      }
+    }
+  };
+
+  while (true) {
+    const int64_t el = s_tk[buf];
+    if (el >= nE) break;
+    if (tid == 0) {  // next ticket now, so its latency hides behind this element
+      const int tn = int(atomicAdd(ticket, 1u));
+      if (tn == total_tickets - 1) atomicExch(ticket, 0u);
+      s_tk[buf ^ 1] = tn;
+    }
+    {  // this element's geometry -> L2
+      const char* gbase = reinterpret_cast<const char*>(geom + el * 6 * NLOC);
+      constexpr int lines = (6 * NLOC * int(sizeof(double)) + 127) / 128;
+      for (int l = tid; l < lines; l += NT) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + size_t(l) * 128));
+    }
+    int ex, ey, ez;
+    coords(el, ex, ey, ez);
+    const int64_t x = int64_t(ex) * q + i, y = int64_t(ey) * q + j, zb = int64_t(ez) * q;
+    double ureg[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const double raw = __ldg(&u[sl.lidx(x, y, zb + k)]);
+      const double v = sl.masked(x, y, zb + k) ? 0.0 : raw;
+      ureg[k] = v;
+      s_a[k * ND2 + ij] = v;
+    }
+    __syncthreads();
+    double ur[ND], us[ND], ut[ND];
+    {
+      double Di[ND], Dj[ND];
+#pragma unroll
+      for (int m = 0; m < ND; ++m) {
+        Di[m] = s_D[i + ND * m];
+        Dj[m] = s_D[j + ND * m];
+      }
+#pragma unroll
+      for (int k = 0; k < ND; ++k) {
+        double dr = 0.0, ds = 0.0, dt = 0.0;
+#pragma unroll
+        for (int m = 0; m < ND; ++m) {
+          dr = fma(Di[m], s_a[k * ND2 + j * ND + m], dr);
+          ds = fma(Dj[m], s_a[k * ND2 + m * ND + i], ds);
+          dt = fma(Dm.d[k + ND * m], ureg[m], dt);
+        }
+        ur[k] = dr;
+        us[k] = ds;
+        ut[k] = dt;
+      }
+    }
+    const double* gg = geom + el * 6 * NLOC + ij;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const int node = k * ND2;
+      double g0, g1, g2, g3, g4, g5;
+      if (el >= 0) {  // always true: keeps per-layer load batches (bounded registers)
+        g0 = __ldcs(gg + 0 * NLOC + node);
+        g1 = __ldcs(gg + 1 * NLOC + node);
+        g2 = __ldcs(gg + 2 * NLOC + node);
+        g3 = __ldcs(gg + 3 * NLOC + node);
+        g4 = __ldcs(gg + 4 * NLOC + node);
+        g5 = __ldcs(gg + 5 * NLOC + node);
+      } else {
+        g0 = g1 = g2 = g3 = g4 = g5 = 0.0;
+      }
+      const double r = ur[k], s = us[k], t = ut[k];
+      ur[k] = g0 * r + g1 * s + g2 * t;
+      us[k] = g1 * r + g3 * s + g4 * t;
+      ut[k] = g2 * r + g4 * s + g5 * t;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      s_a[k * ND2 + ij] = ur[k];
+      s_b[k * ND2 + ij] = us[k];
+    }
+    __syncthreads();
+    double* cur_out = s_out[buf];
+    {
+      double DiT[ND], DjT[ND];
+#pragma unroll
+      for (int m = 0; m < ND; ++m) {
+        DiT[m] = s_D[m + ND * i];
+        DjT[m] = s_D[m + ND * j];
+      }
+      const bool ownx = (i < q) || (ex == sl.Ex - 1), owny = (j < q) || (ey == sl.Ey - 1);
+      const bool topz = (ez == sl.ez1 - 1);
+      const bool hx = (i == 0 && ex > 0), hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
+#pragma unroll
+      for (int k = 0; k < ND; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < ND; ++m) {
+          acc = fma(DiT[m], s_a[k * ND2 + j * ND + m], acc);
+          acc = fma(DjT[m], s_b[k * ND2 + m * ND + i], acc);
+          acc = fma(Dm.d[m + ND * k], ut[m], acc);
+        }
+        const bool own = ownx && owny && (k < q || topz);
+        if (!own) {
+          dep[el * NLOC + k * ND2 + ij] = acc;
+        } else if (hx || hy || (k == 0 && hz)) {
+          cur_out[k * ND2 + ij] = acc;  // owned face node: summed once the neighbours are in
+        } else {
+          const int64_t z = zb + k;  // owned node with no lower contributor: done now
+          epi(sl.lidx(x, y, z), sl.masked(x, y, z) ? 0.0 : acc);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) st_release(&flags[el], target);
+    if (prev >= 0) finish_prev(prev, s_out[buf ^ 1]);
+    prev = el;
+    buf ^= 1;
+    __syncthreads();
+  }
+  if (prev >= 0) finish_prev(prev, s_out[buf ^ 1]);
+}
+
+template <int ND, class EpiT>
+int64_t axp_launch(const Slab& sl, const double* u, const double* geom, const AxSync& sy, const EpiT& epi,
+                   cudaStream_t s) {
+  constexpr int NLOC = ND * ND * ND;
+  const int64_t nE = sl.elems();
+  if (nE == 0) return 0;
+  const size_t smem = (size_t(4) * NLOC + ND * ND) * sizeof(double);
+  auto kern = k_axp<ND, EpiT>;
+  static int nctas = 0;  // resident CTAs: occupancy x SMs (per instantiation)
+  if (nctas == 0) {
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0, dev = 0, sms = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ND * ND, smem));
+    SB_CUDA(cudaGetDevice(&dev));
+    SB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    nctas = std::max(1, per_sm * sms);
+  }
+  const int grid = int(std::min<int64_t>(nctas, nE));
+  kern<<<grid, ND * ND, smem, s>>>(sl, dmat<ND>(sl.q), u, geom, sy.dep, sy.flags, sy.ticket, int(nE + grid), epi);
+  SB_LAUNCH_CHECK();
+  return 1;
+}
+
 template <int ND, bool LOCAL, class EpiT>
 int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, const AxSync& sy, double* out_local,
                        const EpiT& epi, cudaStream_t s) {
+  if constexpr (!LOCAL && ND >= 8) {
+    if (ax_persistent()) return axp_launch<ND>(sl, u, geom, sy, epi, s);
+  }
   constexpr int EPB = epb<ND>();
   constexpr int NLOC = ND * ND * ND;
   const int64_t nE = sl.elems();
