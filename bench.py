@@ -161,7 +161,11 @@ def run_ours(args, cfg, name):
     stream = torch.cuda.Stream(local)
     torch.cuda.set_stream(stream)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # torch.distributed is plumbing only (NCCL id broadcast, barriers, max-over-ranks of the
+        # event timings): gloo on the host. The data path (interface sums, halos, Krylov
+        # allreduces) is the library's own NCCL communicator over NVLink; a second NCCL
+        # communicator from torch would only compete with it.
+        dist.init_process_group("gloo")
         uid = [S.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx = S.Context(local, stream, rank, world, uid[0])
@@ -214,7 +218,7 @@ def run_ours(args, cfg, name):
     launches = ctx.launch_count - launches0
     t = ev0.elapsed_time(ev1) * 1e-3
     if world > 1:
-        tt = torch.tensor([t], device="cuda")
+        tt = torch.tensor([t], dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = tt.item()
     value = n_global * iters / t / 1e9
@@ -239,7 +243,7 @@ def run_ours(args, cfg, name):
     torch.cuda.synchronize()
     t2 = ev2.elapsed_time(ev3) * 1e-3
     if world > 1:
-        tt = torch.tensor([t2], device="cuda")
+        tt = torch.tensor([t2], dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t2 = tt.item()
     e2e = {"value": n_global * it2 / t2 / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * sp.n,
