@@ -11,7 +11,7 @@ LIB := $(PKG)/libsemlab_b200.so
 
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --extended-lambda -Xcompiler -fPIC,-fopenmp \
-           -I$(SRC) -Iinclude
+           -I$(SRC) -Iinclude $(EXTRA)
 CXXFLAGS := -O3 -std=gnu++17 -fPIC -fopenmp -Wall -Wno-unused-function -I$(SRC) -Iinclude -I$(CUDA_HOME)/include
 
 CU_SRCS := $(wildcard $(SRC)/*.cu)

@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsemlab_b200.so")
+# SEMLAB_LIB selects another in-tree build of the same C-ABI (A/B timing of kernel variants)
+LIB_PATH = os.path.join(_HERE, os.environ.get("SEMLAB_LIB", "libsemlab_b200.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -34,13 +34,23 @@ __device__ __forceinline__ void finish_partials(double (&acc)[NC], int ncol, dou
     last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x < ncol) {
-    __threadfence();
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&partial[b * kMaxCol + threadIdx.x]);
-    out[threadIdx.x] = s;
+  if (!last) return;
+  // the whole last block reduces the partials: fixed strided shape, then a block sum
+  __threadfence();
+  double s[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) s[c] = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += kNT)
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < ncol) s[c] += __ldcg(&partial[b * kMaxCol + c]);
+  block_sum<NC, kNT>(s, sred);
+  if (threadIdx.x < NC && threadIdx.x < ncol) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c == int(threadIdx.x)) out[c] = s[c];
   }
-  if (last && threadIdx.x == 0) *counter = 0u;
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 // h = V^T w over the owned range

@@ -23,6 +23,13 @@
 #include "host_math.hpp"
 #include "kernels.hpp"
 
+#ifndef SEMLAB_AX_BATCH_EPI
+#define SEMLAB_AX_BATCH_EPI 1  // owner epilogue: issue all vector loads before the stores
+#endif
+#ifndef SEMLAB_AXP_MINB
+#define SEMLAB_AXP_MINB 8  // resident CTAs per SM the persistent Ax is register-capped for
+#endif
+
 namespace sb {
 
 namespace {
@@ -48,14 +55,24 @@ constexpr int epb() {
 int grid1d(int64_t n, int nt) { return int(std::min<int64_t>((n + nt - 1) / nt, 148LL * 64)); }
 
 // ------------------------------------------------------------------------ epilogues
+// Each epilogue splits into load (vector inputs at node g) and store (combine with (A u)[g]) so
+// a thread can issue the loads of all its nodes before the first store.
 struct EWrite {
   double* w;
-  __device__ void operator()(int64_t g, double v) const { w[g] = v; }
+  struct In {};
+  __device__ In load(int64_t) const { return {}; }
+  __device__ void store(int64_t g, const In&, double v) const { w[g] = v; }
+  __device__ void operator()(int64_t g, double v) const { store(g, load(g), v); }
 };
 struct EResidual {
   double* w;
   const double* b;
-  __device__ void operator()(int64_t g, double v) const { w[g] = b[g] - v; }
+  struct In {
+    double b;
+  };
+  __device__ In load(int64_t g) const { return {b[g]}; }
+  __device__ void store(int64_t g, const In& in, double v) const { w[g] = in.b - v; }
+  __device__ void operator()(int64_t g, double v) const { store(g, load(g), v); }
 };
 struct EChebJacStep {  // chebyshev.cpp:86-92 with S = diag(A)^-1 fused at the owner
   double* x;
@@ -63,13 +80,17 @@ struct EChebJacStep {  // chebyshev.cpp:86-92 with S = diag(A)^-1 fused at the o
   double* d;
   const double* inv;
   double c1, c2;
-  __device__ void operator()(int64_t g, double v) const {
-    const double dg = d[g];
-    x[g] += dg;
-    const double rg = r[g] - inv[g] * v;
+  struct In {
+    double d, x, r, inv;
+  };
+  __device__ In load(int64_t g) const { return {d[g], x[g], r[g], inv[g]}; }
+  __device__ void store(int64_t g, const In& in, double v) const {
+    x[g] = in.x + in.d;
+    const double rg = in.r - in.inv * v;
     r[g] = rg;
-    d[g] = c1 * dg + c2 * rg;
+    d[g] = c1 * in.d + c2 * rg;
   }
+  __device__ void operator()(int64_t g, double v) const { store(g, load(g), v); }
 };
 struct EChebJacInit {  // chebyshev.cpp:80-84: r = S(b - A x); d = r / theta
   double* r;
@@ -77,11 +98,16 @@ struct EChebJacInit {  // chebyshev.cpp:80-84: r = S(b - A x); d = r / theta
   const double* b;
   const double* inv;
   double theta;
-  __device__ void operator()(int64_t g, double v) const {
-    const double rg = inv[g] * (b[g] - v);
+  struct In {
+    double b, inv;
+  };
+  __device__ In load(int64_t g) const { return {b[g], inv[g]}; }
+  __device__ void store(int64_t g, const In& in, double v) const {
+    const double rg = in.inv * (in.b - v);
     r[g] = rg;
     d[g] = rg / theta;
   }
+  __device__ void operator()(int64_t g, double v) const { store(g, load(g), v); }
 };
 
 // ------------------------------------------------------------------------ geometry
@@ -385,7 +411,7 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
 // owned face nodes, whose lower neighbours have long been published. The next ticket is taken,
 // and its geometry prefetched to L2, before the current element is computed.
 template <int ND, class EpiT>
-__global__ void __launch_bounds__(ND* ND, 8)
+__global__ void __launch_bounds__(ND* ND, SEMLAB_AXP_MINB)
     k_axp(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const double* __restrict__ geom,
           double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int total_tickets,
           const EpiT epi) {
@@ -561,6 +587,7 @@ __global__ void __launch_bounds__(ND* ND, 8)
       const bool ownx = (i < q) || (ex == sl.Ex - 1), owny = (j < q) || (ey == sl.Ey - 1);
       const bool topz = (ez == sl.ez1 - 1);
       const bool hx = (i == 0 && ex > 0), hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
+      double outk[ND];
 #pragma unroll
       for (int k = 0; k < ND; ++k) {
         double acc = 0.0;
@@ -570,14 +597,31 @@ __global__ void __launch_bounds__(ND* ND, 8)
           acc = fma(DjT[m], s_b[k * ND2 + m * ND + i], acc);
           acc = fma(Dm.d[m + ND * k], ut[m], acc);
         }
+        outk[k] = acc;
+      }
+      // owned nodes with no lower contributor are final now: batched epilogue (all vector
+      // loads first, then the stores); face-owned nodes wait in smem; the rest are deposited
+      typename EpiT::In in[ND];
+#if SEMLAB_AX_BATCH_EPI
+#pragma unroll
+      for (int k = 0; k < ND; ++k) {
+        const bool own = ownx && owny && (k < q || topz);
+        if (own && !(hx || hy || (k == 0 && hz))) in[k] = epi.load(sl.lidx(x, y, zb + k));
+      }
+#endif
+#pragma unroll
+      for (int k = 0; k < ND; ++k) {
         const bool own = ownx && owny && (k < q || topz);
         if (!own) {
-          dep[el * NLOC + k * ND2 + ij] = acc;
+          dep[el * NLOC + k * ND2 + ij] = outk[k];
         } else if (hx || hy || (k == 0 && hz)) {
-          cur_out[k * ND2 + ij] = acc;  // owned face node: summed once the neighbours are in
+          cur_out[k * ND2 + ij] = outk[k];  // owned face node: summed once the neighbours are in
         } else {
-          const int64_t z = zb + k;  // owned node with no lower contributor: done now
-          epi(sl.lidx(x, y, z), sl.masked(x, y, z) ? 0.0 : acc);
+          const int64_t z = zb + k;
+#if !SEMLAB_AX_BATCH_EPI
+          in[k] = epi.load(sl.lidx(x, y, z));
+#endif
+          epi.store(sl.lidx(x, y, z), in[k], sl.masked(x, y, z) ? 0.0 : outk[k]);
         }
       }
     }
@@ -805,12 +849,18 @@ __global__ void __launch_bounds__(256) k_dots(const DotArgs<K> args, int64_t n, 
     last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x < K) {
-    __threadfence();
-    double s = 0.0;
-    for (unsigned bidx = 0; bidx < gridDim.x; ++bidx) s += __ldcg(&partial[bidx * K + threadIdx.x]);
-    out[threadIdx.x] = s;
-    if (threadIdx.x == 0) *counter = 0u;
+  if (!last) return;
+  __threadfence();  // the whole last block reduces the partials (fixed strided shape)
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = 0.0;
+  for (unsigned bidx = threadIdx.x; bidx < gridDim.x; bidx += 256)
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] += __ldcg(&partial[bidx * K + k]);
+  block_sum<K, 256>(v, sred);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = v[k];
+    *counter = 0u;
   }
 }
 

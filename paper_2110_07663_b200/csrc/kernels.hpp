@@ -66,7 +66,7 @@ struct DotScratch {
   double* partial = nullptr;  // >= kMaxDotBlocks * 32
   unsigned* counter = nullptr;
 };
-constexpr int kMaxDotBlocks = 296;
+constexpr int kMaxDotBlocks = 148 * 8;  // enough CTAs in flight to stream at HBM rate
 int64_t launch_dots(int K, const double* const* a, const double* const* b, int64_t n, double* d_out,
                     const DotScratch& ws, cudaStream_t s);
 

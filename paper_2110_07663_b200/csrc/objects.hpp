@@ -22,6 +22,10 @@ struct semlab_ctx_s {
   sb::DevBuf<unsigned> dot_counter;
   sb::DevBuf<double> dot_out;
   double* host_pinned = nullptr;  // 64 doubles
+  // Krylov workspace kept across solves (grow-only): cudaMalloc/cudaFree of the ~2 GB GMRES basis
+  // per solve costs a device sync and tens to hundreds of ms. A nested solve allocates its own.
+  sb::DevBuf<double> krylov_ws;
+  bool krylov_ws_busy = false;
   sb::DotScratch dots() const { return {dot_partial.p, dot_counter.p}; }
   void count(int64_t n) { launches += n; }
   // Global sum over ranks of K host doubles (NCCL allreduce on device values when nranks>1).

@@ -239,6 +239,36 @@ semlab_lambda_estimate estimate_lambda_max(semlab_op S, semlab_op A, int64_t n, 
   return est;
 }
 
+namespace {
+
+// Columns of the Krylov workspace start on 256-byte boundaries.
+int64_t padded(int64_t n) { return (n + 31) / 32 * 32; }
+
+// The context's persistent workspace for the duration of one solve.
+struct WsLease {
+  semlab_ctx c;
+  DevBuf<double> own;
+  double* p = nullptr;
+  bool leased = false;
+  WsLease(semlab_ctx c_, size_t count) : c(c_) {
+    if (!c->krylov_ws_busy) {
+      if (c->krylov_ws.n < count) c->krylov_ws.alloc(count);
+      c->krylov_ws_busy = leased = true;
+      p = c->krylov_ws.p;
+    } else {
+      own.alloc(count);
+      p = own.p;
+    }
+  }
+  ~WsLease() {
+    if (leased) c->krylov_ws_busy = false;
+  }
+  WsLease(const WsLease&) = delete;
+  WsLease& operator=(const WsLease&) = delete;
+};
+
+}  // namespace
+
 KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, const semlab_gmres_config& cfg) {
   if (cfg.restart < 1) invalid("gmres: restart must be >= 1");
   if (cfg.restart > 31) invalid("gmres: restart must be <= 31 on the device path");
@@ -250,7 +280,11 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
   const int m = cfg.restart;
   const OwnRange o = own_range_of(A);
   KrylovResult res;
-  DevBuf<double> r(static_cast<size_t>(n)), w(static_cast<size_t>(n)), z(static_cast<size_t>(n)), V(size_t(n) * (m + 1)), dh(96);
+  const int64_t ld = padded(n);
+  WsLease ws(c, size_t(ld) * (m + 4) + 96);
+  struct {
+    double* p;
+  } r{ws.p}, w{ws.p + ld}, z{ws.p + 2 * ld}, V{ws.p + 3 * ld}, dh{ws.p + size_t(ld) * (m + 4)};
   auto applyM = [&](const double* in, double* out) {
     if (M)
       M->apply(in, out);
@@ -286,10 +320,10 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
     int j = 0;
     bool lucky = false;
     for (; j < m && res.iterations < cfg.max_iters; ++j) {
-      applyM(V.p + size_t(j) * n, z.p);
+      applyM(V.p + size_t(j) * ld, z.p);
       A->apply(z.p, w.p);
       double hnext = 0.0;
-      cgs2(c, o, V.p, n, j + 1, w.p, dh.p, h, hnext);
+      cgs2(c, o, V.p, ld, j + 1, w.p, dh.p, h, hnext);
       for (int i = 0; i <= j; ++i) Hc(i, j) = h[size_t(i)];
       Hc(j + 1, j) = hnext;
       for (int i = 0; i < j; ++i) {  // Givens (krylov.cpp:77-89)
@@ -313,7 +347,7 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
         ++j;
         break;
       }
-      c->count(launch_div(V.p + size_t(j + 1) * n, w.p, hnext, n, s));
+      c->count(launch_div(V.p + size_t(j + 1) * ld, w.p, hnext, n, s));
       if (res_est <= target) {
         ++j;
         break;
@@ -326,7 +360,7 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
         for (int k = i + 1; k < j; ++k) acc -= Hc(i, k) * y[size_t(k)];
         y[size_t(i)] = acc / Hc(i, i);
       }
-      c->count(launch_gemv_n(V.p, n, j, y.data(), w.p, n, s));
+      c->count(launch_gemv_n(V.p, ld, j, y.data(), w.p, n, s));
       applyM(w.p, z.p);
       c->count(launch_axpby(x, 1.0, z.p, 1.0, n, s));
     }
@@ -352,7 +386,11 @@ KrylovResult pcg_solve(semlab_op A, semlab_op M, const double* b, double* x, con
   const int64_t n = A->n;
   const OwnRange o = own_range_of(A);
   KrylovResult res;
-  DevBuf<double> r(static_cast<size_t>(n)), w(static_cast<size_t>(n)), z(static_cast<size_t>(n)), p(static_cast<size_t>(n));
+  const int64_t ld = padded(n);
+  WsLease ws(c, size_t(ld) * 4);
+  struct {
+    double* p;
+  } r{ws.p}, w{ws.p + ld}, z{ws.p + 2 * ld}, p{ws.p + 3 * ld};
   auto dot = [&](const double* a, const double* bb) {
     const double* av[1] = {a};
     const double* bv[1] = {bb};

@@ -63,6 +63,8 @@ def main():
     A = pmg.spaces[0].as_linop()
     M = pmg.as_linop()
     x = torch.zeros_like(b)
+    S.gmres_solve(A, M, b, x, S.GmresConfig())  # warm (basis allocation, first launches)
+    x.zero_()
     torch.cuda.synchronize()
     t0 = time.time()
     st = S.gmres_solve(A, M, b, x, S.GmresConfig())
