@@ -208,6 +208,7 @@ def run_ours(args, cfg, name):
         barrier()
         ev0.record(stream)
         step_ms = []
+        torch.cuda.nvtx.range_push("timed")  # lets `ncu --nvtx --nvtx-include timed/` list exactly these launches
         for _ in range(args.steps):
             ts = time.perf_counter()
             st = step()
@@ -215,6 +216,7 @@ def run_ours(args, cfg, name):
             iters += st.iterations
             conv = conv and st.converged
             rel = max(rel, st.rel_residual)
+        torch.cuda.nvtx.range_pop()
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()

@@ -23,34 +23,48 @@ __device__ __forceinline__ bool on_boundary(int64_t x, int64_t y, int64_t z, con
   return x == 0 || x == g.N[0] - 1 || y == 0 || y == g.N[1] - 1 || z == 0 || z == g.N[2] - 1;
 }
 
-// One 1-D pass along `axis`. in/out are (x,y,z) arrays, x fastest, with local z offsets.
+// One 1-D pass along AXIS. in/out are (x,y,z) arrays, x fastest, with local z offsets.
 // PROLONG: out[X] = sum_a J(i(X), a) in[e(X) qc + a]
 // RESTRICT: out[I] = sum over the 1-D support of coarse node I of J(i, a) in[X] (each X once)
-template <bool PROLONG>
-__global__ void k_pass(const double* __restrict__ in, const Grid3 gin, double* __restrict__ out, const Grid3 gout,
-                       const int axis, const Jmat J, const int qf, const int qc, const int E_axis, const int mask_in,
-                       const Grid3 gmask_in, const int mask_out, const Grid3 gmask_out, const int64_t zb,
-                       const int64_t nz) {
-  const int64_t nx = gout.N[0], ny = gout.N[1];
-  const int64_t total = nx * ny * nz;
+// The pass axis is a template parameter and the output coordinates come from 32-bit divisions
+// (the launcher checks the extents), so the index arithmetic stays off the critical path.
+template <bool PROLONG, int AXIS>
+__global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, const Grid3 gin, double* __restrict__ out,
+                                              const Grid3 gout, const Jmat J, const int qf, const int qc,
+                                              const int E_axis, const int mask_in, const Grid3 gmask_in,
+                                              const int mask_out, const Grid3 gmask_out, const int zb, const int nz) {
+  const unsigned nx = unsigned(gout.N[0]), ny = unsigned(gout.N[1]);
+  const unsigned total = nx * ny * unsigned(nz);
   const int jn = qc + 1;  // J is (qf+1) x (qc+1), row-major
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-    int64_t c[3] = {t % nx, (t / nx) % ny, zb + t / (nx * ny)};
-    double acc = 0.0;
+  const int64_t sin = AXIS == 0 ? 1 : (AXIS == 1 ? gin.nxl : gin.nxl * gin.nyl);
+  const int64_t nax_in = gmask_in.N[AXIS];
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const unsigned row = t / nx;
+    const int c[3] = {int(t - row * nx), int(row % ny), zb + int(row / ny)};
     if (mask_out && gmask_out.dirichlet && on_boundary(c[0], c[1], c[2], gmask_out)) {
       out[gout.idx(c[0], c[1], c[2])] = 0.0;
       continue;
     }
-    const int64_t X = c[axis];
-    auto fetch = [&](int64_t coord) -> double {
-      int64_t cc[3] = {c[0], c[1], c[2]};
-      cc[axis] = coord;
-      if (mask_in && gmask_in.dirichlet && on_boundary(cc[0], cc[1], cc[2], gmask_in)) return 0.0;
-      return in[gin.idx(cc[0], cc[1], cc[2])];
+    // input row through this point along AXIS; the other two coordinates fix the mask test
+    int c0[3] = {c[0], c[1], c[2]};
+    c0[AXIS] = 0;
+    const double* row_in = in + gin.idx(c0[0], c0[1], c0[2]);
+    bool other_bnd = false;
+    if (mask_in && gmask_in.dirichlet) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (d != AXIS) other_bnd = other_bnd || c[d] == 0 || c[d] == gmask_in.N[d] - 1;
+    }
+    const bool min_ = mask_in && gmask_in.dirichlet;
+    auto fetch = [&](int coord) -> double {
+      if (min_ && (other_bnd || coord == 0 || coord == nax_in - 1)) return 0.0;
+      return row_in[coord * sin];
     };
+    const int X = c[AXIS];
+    double acc = 0.0;
     if (PROLONG) {
-      int64_t e = X / qf;
-      int i = int(X - e * qf);
+      int e = X / qf;
+      int i = X - e * qf;
       if (e == E_axis) {
         e -= 1;
         i = qf;
@@ -60,9 +74,9 @@ __global__ void k_pass(const double* __restrict__ in, const Grid3 gin, double* _
         if (w != 0.0) acc += w * fetch(e * qc + a);
       }
     } else {
-      const int64_t I = X;
-      int64_t e = I / qc;
-      const int a = int(I - e * qc);
+      const int I = X;
+      int e = I / qc;
+      const int a = I - e * qc;
       if (a == 0 && e > 0) {  // shared coarse node: left element (a' = qc), then right element
         // (on a slab, an element of the other rank contributes through the interface sum; the
         // shared fine node X = e qf is counted with the left element only)
@@ -77,10 +91,8 @@ __global__ void k_pass(const double* __restrict__ in, const Grid3 gin, double* _
             if (w != 0.0) acc += w * fetch(e * qf + i);
           }
       } else {
-        if (e == E_axis) {  // last coarse node belongs to the last element
-          e -= 1;
-        }
-        const int aa = int(I - e * qc);
+        if (e == E_axis) e -= 1;  // last coarse node belongs to the last element
+        const int aa = I - e * qc;
         for (int i = 0; i <= qf; ++i) {
           const double w = J.v[i * jn + aa];
           if (w != 0.0) acc += w * fetch(e * qf + i);
@@ -98,12 +110,18 @@ int64_t launch_transfer_pass(bool prolong, const double* in, const Grid3& gin, d
                              bool mask_out, const Grid3& gmo, int64_t zb, int64_t nz, cudaStream_t s) {
   const int64_t total = gout.N[0] * gout.N[1] * nz;
   if (total <= 0) return 0;
-  if (prolong)
-    k_pass<true><<<grid_for(total), 256, 0, s>>>(in, gin, out, gout, axis, J, qf, qc, E_axis, mask_in, gmi, mask_out,
-                                                 gmo, zb, nz);
-  else
-    k_pass<false><<<grid_for(total), 256, 0, s>>>(in, gin, out, gout, axis, J, qf, qc, E_axis, mask_in, gmi,
-                                                  mask_out, gmo, zb, nz);
+  if (total >= (int64_t(1) << 32) || gmi.N[2] >= (int64_t(1) << 31) || zb >= (int64_t(1) << 31))
+    invalid("transfer pass: lattice too large for 32-bit pass indexing");
+  if (axis < 0 || axis > 2) invalid("transfer pass: axis must be 0, 1 or 2");
+#define L_(PR, AX)                                                                                            \
+  k_pass<PR, AX><<<grid_for(total), 256, 0, s>>>(in, gin, out, gout, J, qf, qc, E_axis, mask_in, gmi, mask_out, \
+                                                  gmo, int(zb), int(nz))
+  if (prolong) {
+    if (axis == 0) L_(true, 0); else if (axis == 1) L_(true, 1); else L_(true, 2);
+  } else {
+    if (axis == 0) L_(false, 0); else if (axis == 1) L_(false, 1); else L_(false, 2);
+  }
+#undef L_
   SB_LAUNCH_CHECK();
   return 1;
 }

@@ -183,7 +183,7 @@ bool ax_persistent() {
 
 template <int ND>
 constexpr int ax_min_blocks() {  // occupancy target: caps registers so ~20 warps/SM stay resident
-  return ND >= 8 ? 10 : 4;
+  return ND >= 8 ? 10 : 16;
 }
 
 template <int ND, int EPB, bool LOCAL, class EpiT>

@@ -1,14 +1,20 @@
 #!/bin/bash
-# Runs on the GPU box: plain bench, launch list, and full ncu captures of the top kernels.
+# Runs on the GPU box (one GPU): the default bench line, the ncu launch list of the bench command
+# (per-launch times, cold cache, serialised) and one --set full capture of the top kernels.
+# Outputs land in gpurun_out/; tools/profile_summary.py turns them into profiles/<round>_*.
+R=${ROUND:-r01}
 set -x
 mkdir -p gpurun_out
-python bench.py --steps 2 --warmup 3 > gpurun_out/bench.log 2>&1 || exit 1
-tail -1 gpurun_out/bench.log
+if [ "${FULL_ONLY:-0}" = "0" ]; then
+  python bench.py > gpurun_out/bench_$R.log 2>&1 || exit 1
+  tail -1 gpurun_out/bench_$R.log
+  ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" --csv \
+      --log-file gpurun_out/launches_$R.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+      > gpurun_out/ncu_launches_$R.log 2>&1
+fi
 if [ "${NCU:-1}" = "1" ]; then
-  python tools/perf_probe.py --E 32 --solve 1 > gpurun_out/probe_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:'k_axp|k_ras' -s 12 -c 6 \
-      -o gpurun_out/prof_top -f python tools/perf_probe.py --E 32 --solve 1 > gpurun_out/ncu_full.log 2>&1
-  ncu --metrics gpu__time_duration.sum --clock-control none -s 2500 -c 3000 --csv \
-      --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
+  ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k regex:"${KREGEX:-k_axp|k_ras<\(int\)10|k_pass|k_cgs_update_dot|k_gemv_t}" -s ${SKIP:-60} -c ${COUNT:-16} \
+      --nvtx --nvtx-include "timed/" -o gpurun_out/full_$R${TAG:-} -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_$R${TAG:-}.log 2>&1
 fi
 exit 0
