@@ -14,11 +14,23 @@
 // vector update. ASM: per-element boxes go to a buffer and every node sums the boxes covering it
 // in ascending element id (the reference's order) times 1/count (schwarz.cpp:269-287).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_set>
 
 #include "device.cuh"
 #include "kernels_fdm.hpp"
+
+#ifndef SEMLAB_RASW_GATHER_UNROLL
+#define SEMLAB_RASW_GATHER_UNROLL 2  // z-columns of the box gathered per lane per batch
+#endif
+#ifndef SEMLAB_RASW_OWNER_U
+#define SEMLAB_RASW_OWNER_U 4  // owned sites per lane per batch of the owner write
+#endif
+constexpr int kGatherUnroll = SEMLAB_RASW_GATHER_UNROLL;
+#ifndef SEMLAB_RASW_MINB
+#define SEMLAB_RASW_MINB 5  // resident 4-warp CTAs per SM the warp-per-element RAS is register-capped for
+#endif
 
 namespace sb {
 
@@ -57,7 +69,14 @@ struct Shape {
   static constexpr size_t smem() { return size_t(EPC) * SPE * sizeof(T); }
 };
 
-__device__ __forceinline__ float rcp(float s) { return __frcp_rn(s); }
+// 1/s for the FP32 smoother: hardware approximation plus one Newton step (within 1 ulp of the
+// rounded quotient; s = lx + ly + lz > 0 is a normal number), three instructions instead of the
+// special-case-checking IEEE sequence
+__device__ __forceinline__ float rcp(float s) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
+  return fmaf(r, fmaf(-s, r, 1.0f), r);
+}
 __device__ __forceinline__ double rcp(double s) { return 1.0 / s; }
 
 // One line pass along axis AX: for the thread's R lines, out = M^T in (FWD) or M in (!FWD);
@@ -331,6 +350,294 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_ras(const Slab 
   }
 }
 
+// ---------------------------------------------------------------- RAS, one warp per element
+// Same arithmetic (and summation order) as k_ras, organised so no CTA barrier couples elements:
+// each warp owns one element at a time in a grid-stride loop and synchronises with __syncwarp
+// only, so the gather, the FMA passes and the owner write of different warps overlap freely.
+// Gather and owner write walk the box / owned sites with x fastest across the lanes (coalesced
+// runs); the line passes stream the input lines from shared memory (accumulators in registers,
+// ~100 registers) so five CTAs of four warps fit per SM.
+template <int P, class T>
+struct WShape {
+  static constexpr int P2 = P * P, P3 = P2 * P;
+  static constexpr int R = (P2 + 31) / 32;  // lines per lane
+  static constexpr int WPC = 4;             // warps (elements in flight) per CTA
+  static constexpr int NT = 32 * WPC;
+  static constexpr int SPE = (2 * P3 + 3 * P2 + 3 * P + 3) / 4 * 4;  // box, tmp, S, L (16B multiple)
+  static constexpr size_t smem() { return size_t(WPC) * SPE * sizeof(T); }
+};
+
+template <int P, int AX>
+__device__ __forceinline__ int wline_base(int l) {
+  constexpr int P2 = P * P;
+  const int u = l % P, v = l / P;
+  return AX == 0 ? (v * P2 + u * P) : (AX == 1 ? (v * P2 + u) : (v * P + u));
+}
+
+template <int P, class T>
+__device__ __forceinline__ void load_pair(const T* M, T& s0, T& s1) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 v = *reinterpret_cast<const float2*>(M);
+    s0 = v.x;
+    s1 = v.y;
+  } else {
+    const double2 v = *reinterpret_cast<const double2*>(M);
+    s0 = v.x;
+    s1 = v.y;
+  }
+}
+
+// forward transform along AX: y[o] = sum_a M(a,o) x[a], x streamed from src, y in registers
+template <int P, class T, int AX>
+__device__ __forceinline__ void wfwd(const T* __restrict__ src, const T* __restrict__ M, const int (&base)[WShape<P, T>::R],
+                                     T (&y)[WShape<P, T>::R][P]) {
+  constexpr int R = WShape<P, T>::R;
+  constexpr int stride = AX == 0 ? 1 : (AX == 1 ? P : P * P);
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int o = 0; o < P; ++o) y[r][o] = T(0);
+#pragma unroll 2  // bounded: a full unroll hoists every S load and spills
+  for (int a = 0; a < P; ++a) {
+    T xa[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) xa[r] = src[base[r] + a * stride];
+    if constexpr (P % 2 == 0) {
+#pragma unroll
+      for (int o = 0; o < P; o += 2) {
+        T s0, s1;
+        load_pair<P, T>(M + a * P + o, s0, s1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          y[r][o] = fma(s0, xa[r], y[r][o]);
+          y[r][o + 1] = fma(s1, xa[r], y[r][o + 1]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < P; ++o) {
+        const T sv = M[a * P + o];
+#pragma unroll
+        for (int r = 0; r < R; ++r) y[r][o] = fma(sv, xa[r], y[r][o]);
+      }
+    }
+  }
+}
+
+// backward transform along AX: dst[a] = sum_o M(a,o) x[o], x in registers, rows written as formed
+template <int P, class T, int AX>
+__device__ __forceinline__ void wbwd(const T (&x)[WShape<P, T>::R][P], const T* __restrict__ M,
+                                     const int (&base)[WShape<P, T>::R], const bool (&ok)[WShape<P, T>::R],
+                                     T* __restrict__ dst) {
+  constexpr int R = WShape<P, T>::R;
+  constexpr int stride = AX == 0 ? 1 : (AX == 1 ? P : P * P);
+#pragma unroll 2
+  for (int a = 0; a < P; ++a) {
+    T acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = T(0);
+    if constexpr (P % 2 == 0) {
+#pragma unroll
+      for (int o = 0; o < P; o += 2) {
+        T s0, s1;
+        load_pair<P, T>(M + a * P + o, s0, s1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r] = fma(s0, x[r][o], acc[r]);
+          acc[r] = fma(s1, x[r][o + 1], acc[r]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < P; ++o) {
+        const T sv = M[a * P + o];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = fma(sv, x[r][o], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (ok[r]) dst[base[r] + a * stride] = acc[r];
+  }
+}
+
+template <int P, class T, int AX>
+__device__ __forceinline__ void wbases(int lane, int (&base)[WShape<P, T>::R], bool (&ok)[WShape<P, T>::R]) {
+#pragma unroll
+  for (int r = 0; r < WShape<P, T>::R; ++r) {
+    const int l = lane + 32 * r;
+    ok[r] = l < P * P;
+    base[r] = ok[r] ? wline_base<P, AX>(l) : 0;  // idle lines read a valid address, never write
+  }
+}
+
+template <int P, class T, int MODE>
+__global__ void __launch_bounds__(WShape<P, T>::NT, sizeof(T) == 4 ? SEMLAB_RASW_MINB : 2)
+    k_rasw(const Slab sl, const T* __restrict__ S, const T* __restrict__ L, const double* __restrict__ rin,
+           RasEpi epi) {
+  using W = WShape<P, T>;
+  constexpr int P2 = W::P2, P3 = W::P3, R = W::R, SPE = W::SPE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* box = reinterpret_cast<T*>(smem_raw) + warp * SPE;
+  T* tmp = box + P3;
+  T* Se = tmp + P3;
+  T* Le = Se + 3 * P2;
+  const int nE = int(sl.elems());
+  const bool dir = sl.dirichlet != 0;
+  for (int el = blockIdx.x * W::WPC + warp; el < nE; el += gridDim.x * W::WPC) {
+    const int ex = el % sl.Ex, ey = (el / sl.Ex) % sl.Ey, ez = sl.ez0 + el / (sl.Ex * sl.Ey);
+    const Box1D X = box1d(ex, sl.Ex, sl.q, dir), Y = box1d(ey, sl.Ey, sl.q, dir), Z = box1d(ez, sl.Ez, sl.q, dir);
+    __syncwarp();  // the previous element's owner write has finished reading tmp
+    {  // factors: S (3 P^2) and lambda (3 P), all loads issued before the stores
+      constexpr int NF = 3 * P2 + 3 * P, IT = (NF + 31) / 32;
+      T v[IT];
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int w = lane + 32 * it;
+        v[it] = w < 3 * P2 ? __ldg(S + int64_t(el) * 3 * P2 + w)
+                           : (w < NF ? __ldg(L + int64_t(el) * 3 * P + (w - 3 * P2)) : T(0));
+      }
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int w = lane + 32 * it;
+        if (w < NF) Se[w] = v[it];
+      }
+    }
+    {  // gather the extended box by z-columns: lane = (a, b) pair, loop over c, so the x/y
+       // validity and the column address are fixed per pair and the z test is a bit mask; sites
+       // outside the core in more than one direction (and outside a smaller boundary box) are zero
+       // (schwarz.cpp:255-265)
+      unsigned zin = 0, zcore = 0;  // c < Z.n; c < Z.n and not a z ghost
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        zin |= unsigned(c < Z.n) << c;
+        zcore |= unsigned(c < Z.n && !ghost(Z, c)) << c;
+      }
+      const int64_t NXY = sl.Nx * sl.Ny;
+      const double* corner = rin + sl.lidx(X.lo, Y.lo, Z.lo);
+#pragma unroll kGatherUnroll
+      for (int r = 0; r < R; ++r) {
+        const int l = min(lane + 32 * r, P2 - 1);  // lanes past the last pair redo it (same values)
+        const int a = l % P, b = l / P;
+        const bool okab = a < X.n && b < Y.n;
+        const int gab = int(ghost(X, a)) + int(ghost(Y, b));
+        const unsigned m = !okab ? 0u : (gab == 0 ? zin : (gab == 1 ? zcore : 0u));
+        const double* col = corner + a + b * sl.Nx;
+        double v[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) v[c] = __ldg((m >> c) & 1u ? col + c * NXY : rin);
+#pragma unroll
+        for (int c = 0; c < P; ++c) box[c * P2 + l] = (m >> c) & 1u ? T(v[c]) : T(0);
+      }
+    }
+    __syncwarp();
+    int base[R];
+    bool okl[R];
+    T y[R][P];
+    wbases<P, T, 0>(lane, base, okl);
+    wfwd<P, T, 0>(box, Se + 0 * P2, base, y);  // x forward: box -> tmp
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (okl[r])
+#pragma unroll
+        for (int o = 0; o < P; ++o) tmp[base[r] + o] = y[r][o];
+    __syncwarp();
+    wbases<P, T, 1>(lane, base, okl);
+    wfwd<P, T, 1>(tmp, Se + 1 * P2, base, y);  // y forward: tmp -> box
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (okl[r])
+#pragma unroll
+        for (int o = 0; o < P; ++o) box[base[r] + o * P] = y[r][o];
+    __syncwarp();
+    wbases<P, T, 2>(lane, base, okl);
+    wfwd<P, T, 2>(box, Se + 2 * P2, base, y);  // z forward, scale by inv_D, z backward: box -> tmp
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int l = lane + 32 * r;
+      const int a = l % P, b = (l / P) % P;
+      const T lab = Le[0 * P + a] + Le[1 * P + b];
+#pragma unroll
+      for (int c = 0; c < P; ++c) y[r][c] = y[r][c] * rcp(lab + Le[2 * P + c]);
+    }
+    wbwd<P, T, 2>(y, Se + 2 * P2, base, okl, tmp);
+    __syncwarp();
+    wbases<P, T, 1>(lane, base, okl);  // y backward: tmp -> box
+    {
+      constexpr int stride = P;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int m = 0; m < P; ++m) y[r][m] = tmp[base[r] + m * stride];
+    }
+    wbwd<P, T, 1>(y, Se + 1 * P2, base, okl, box);
+    __syncwarp();
+    wbases<P, T, 0>(lane, base, okl);  // x backward: box -> tmp
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int m = 0; m < P; ++m) y[r][m] = box[base[r] + m];
+    wbwd<P, T, 0>(y, Se + 0 * P2, base, okl, tmp);
+    __syncwarp();
+    // owner write by z-columns: lane = (a, b) over the owned face (QA x QA, power of two so the
+    // split is a shift), U consecutive c per round with every vector load issued before the stores
+    const int na = X.own_hi - X.own_lo + 1, nb = Y.own_hi - Y.own_lo + 1, nc = Z.own_hi - Z.own_lo + 1;
+    constexpr int QA = (P - 2) <= 4 ? 4 : ((P - 2) <= 8 ? 8 : 16);
+    constexpr int U = SEMLAB_RASW_OWNER_U;
+    const int64_t NXY = sl.Nx * sl.Ny;
+#pragma unroll 1
+    for (int pr = lane; pr < QA * QA; pr += 32) {
+      const int oa = pr % QA, ob = pr / QA;
+      if (oa >= na || ob >= nb) continue;
+      const int aa = X.own_lo + oa, bb = Y.own_lo + ob;
+      const int64_t g0 = sl.lidx(X.lo + aa, Y.lo + bb, Z.lo + Z.own_lo);
+      const T* zt = tmp + Z.own_lo * P2 + bb * P + aa;
+#pragma unroll 1
+      for (int c0 = 0; c0 < nc; c0 += U) {
+        int64_t g[U];
+        bool ok[U];
+        double z[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u;
+          ok[u] = c < nc;
+          g[u] = ok[u] ? g0 + c * NXY : g0;
+          z[u] = ok[u] ? double(zt[c * P2]) : 0.0;
+        }
+        if (MODE == 0) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) epi.out[g[u]] = z[u];
+        } else if (MODE == 1) {  // Chebyshev init: r = S t, d = r / theta  (chebyshev.cpp:82-84)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) {
+              epi.r[g[u]] = z[u];
+              epi.d[g[u]] = z[u] / epi.c1;
+            }
+        } else {  // Chebyshev step: x += d; r -= S A d; d = c1 d + c2 r  (chebyshev.cpp:86-92)
+          double dv[U], rv[U], xv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            dv[u] = epi.d[g[u]];
+            rv[u] = epi.r[g[u]];
+            xv[u] = epi.x[g[u]];
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) {
+              epi.x[g[u]] = xv[u] + dv[u];
+              const double rg = rv[u] - z[u];
+              epi.r[g[u]] = rg;
+              epi.d[g[u]] = epi.c1 * dv[u] + epi.c2 * rg;
+            }
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- ASM boxes + deterministic sum
 template <int P, class T>
 __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_asm_boxes(const Slab sl, const T* __restrict__ S, const T* __restrict__ L,
@@ -417,10 +724,41 @@ void prep(K kern, size_t smem) {
     SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
 }
 
+bool ras_warp() {
+  static const bool on = [] {
+    const char* e = std::getenv("SEMLAB_RAS_WARP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class T>
 struct Launch {
+  // warp-per-element RAS for the large boxes (SEMLAB_RAS_WARP=0 selects the CTA-per-group kernel)
+  template <int P, int MODE>
+  static void rasw(const Slab& sl, const T* S, const T* L, const double* r, const RasEpi& e, cudaStream_t s) {
+    using W = WShape<P, T>;
+    auto kern = k_rasw<P, T, MODE>;
+    prep(kern, W::smem());
+    static int per_sm = 0;
+    if (!per_sm) {
+      SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::NT, W::smem()));
+      int dev = 0, sms = 0;
+      SB_CUDA(cudaGetDevice(&dev));
+      SB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      per_sm = std::max(1, per_sm) * sms;
+    }
+    const int64_t need = (sl.elems() + W::WPC - 1) / W::WPC;
+    kern<<<int(std::min<int64_t>(need, per_sm)), W::NT, W::smem(), s>>>(sl, S, L, r, e);
+  }
   template <int P>
   static void ras(const Slab& sl, const T* S, const T* L, const double* r, int mode, const RasEpi& e, cudaStream_t s) {
+    if (sizeof(T) == 4 && P >= 8 && ras_warp() && sl.elems() < (int64_t(1) << 31)) {
+      if (mode == 0) rasw<P, 0>(sl, S, L, r, e, s);
+      else if (mode == 1) rasw<P, 1>(sl, S, L, r, e, s);
+      else rasw<P, 2>(sl, S, L, r, e, s);
+      return;
+    }
     using Sh = Shape<P, T>;
     const int grid = int((sl.elems() + Sh::EPC - 1) / Sh::EPC);
     if (mode == 0) {

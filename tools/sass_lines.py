@@ -1,7 +1,8 @@
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
 ncu's SASS page (addresses + samples) is matched by instruction offset against the line table
 nvdisasm prints for the same locally built object (built with -lineinfo).
-usage: python tools/sass_lines.py REPORT KERNEL_REGEX OBJ MANGLED_SUBSTR [top]"""
+usage: python tools/sass_lines.py REPORT KERNEL_REGEX OBJ MANGLED_SUBSTR [top] [ncu source column]
+(column e.g. "Instructions Executed" for the instruction mix instead of stall samples)"""
 import collections
 import csv
 import re
@@ -14,12 +15,13 @@ import os
 def main():
     rep, kre, obj, mang = sys.argv[1:5]
     top = int(sys.argv[5]) if len(sys.argv) > 5 else 40
+    col = sys.argv[6] if len(sys.argv) > 6 else "Warp Stall Sampling (All Samples)"
     raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass",
                           "--kernel-id", f"::regex:{kre}:1"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     h = rows[hi]
-    si, ai = h.index("Warp Stall Sampling (All Samples)"), h.index("Address")
+    si, ai = h.index(col), h.index("Address")
     samples = []
     for r in rows[hi + 1:]:
         if len(r) > si and r[ai].startswith("0x"):
