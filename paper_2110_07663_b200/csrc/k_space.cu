@@ -27,7 +27,7 @@
 #define SEMLAB_AX_BATCH_EPI 1  // owner epilogue: issue all vector loads before the stores
 #endif
 #ifndef SEMLAB_AXP_MINB
-#define SEMLAB_AXP_MINB 8  // resident CTAs per SM the persistent Ax is register-capped for
+#define SEMLAB_AXP_MINB 6  // resident CTAs per SM the persistent Ax is register-capped for
 #endif
 
 namespace sb {
@@ -404,70 +404,103 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
 }
 
 // ------------------------------------------------------------------------ persistent Ax
-// Same arithmetic and summation order as k_ax, restructured so no CTA idles on a neighbour:
-// a resident CTA loops over dynamic tickets; for ticket t it computes the element, deposits
-// the non-owned nodes, writes the owned nodes that have no lower contributor (the 6^3 interior
-// of a p=7 element) right away and publishes its counter; only then does it finish ticket t-1's
-// owned face nodes, whose lower neighbours have long been published. The next ticket is taken,
-// and its geometry prefetched to L2, before the current element is computed.
-template <int ND, class EpiT>
-__global__ void __launch_bounds__(ND* ND, SEMLAB_AXP_MINB)
-    k_axp(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const double* __restrict__ geom,
+// Same arithmetic and summation order as k_ax, restructured so no CTA idles on a neighbour or
+// on HBM latency. A resident CTA loops over dynamic tickets (ascending element id):
+//   * the element's 6 geometric-factor planes arrive in shared memory by ONE cp.async.bulk
+//     (TMA engine, mbarrier completion) that was issued while the PREVIOUS element was in its
+//     transposed contractions, so the 24 KB stream of each element overlaps a whole element of
+//     compute; no registers or issue slots are spent on geometry loads;
+//   * the next element's u rows are prefetched into L2 while this element is differentiated;
+//   * the element deposits its non-owned nodes, writes the owned nodes with no lower
+//     contributor (the 6^3 interior at p=7) at once, keeps its face-owned results in registers
+//     and publishes its counter; only then does it finish ticket t-1's face-owned nodes, whose
+//     lower neighbours have long been published.
+// All lattice offsets are 32-bit (n_local < 2^31 is checked on the host); masking is
+// precomputed per column (x,y) plus the two z end layers.
+template <class GT>
+__host__ __device__ constexpr int geom_bytes(int nloc) {
+  return 6 * nloc * int(sizeof(GT));
+}
+__host__ __device__ constexpr int align128(int b) { return (b + 127) / 128 * 128; }
+
+#ifndef SEMLAB_AXP_UPREFETCH
+#define SEMLAB_AXP_UPREFETCH 1  // L2 prefetch of the next element's u rows
+#endif
+
+template <int ND>
+constexpr int axp_minb() {  // resident CTAs per SM (shared memory allows no more at ND >= 9)
+  return ND <= 8 ? SEMLAB_AXP_MINB : (ND == 9 ? 4 : 3);
+}
+
+template <int ND, class EpiT, class GT>
+__global__ void __launch_bounds__(ND* ND, axp_minb<ND>())
+    k_axp(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const GT* __restrict__ geom,
           double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int total_tickets,
           const EpiT epi) {
   constexpr int ND2 = ND * ND, NLOC = ND2 * ND, NT = ND2;
   constexpr int q = ND - 1;
+  constexpr unsigned GB = unsigned(geom_bytes<GT>(NLOC));
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* s_a = reinterpret_cast<double*>(smem_raw);
+  GT* s_g = reinterpret_cast<GT*>(smem_raw);
+  double* s_a = reinterpret_cast<double*>(smem_raw + align128(int(GB)));
   double* s_b = s_a + NLOC;
   double* s_D = s_b + NLOC;
-  double* s_out[2] = {s_D + ND2, s_D + ND2 + NLOC};  // per-element results awaiting completion
+  __shared__ uint64_t s_bar;
   __shared__ int s_tk[2];
   __shared__ unsigned s_epoch;
   const int tid = threadIdx.x;
   const int ij = tid, i = ij % ND, j = ij / ND;
-  const int64_t nE = sl.elems();
-  const int64_t LX = 1, LY = sl.Ex, LZ = int64_t(sl.Ex) * sl.Ey;
+  const int nE = int(sl.elems());
+  const int Ex = sl.Ex, Ey = sl.Ey, LZ = Ex * Ey;
+  const int Nx = int(sl.Nx), Ny = int(sl.Ny), Nz = int(sl.Nz), NxNy = Nx * Ny;
+  const int zlo = int(sl.zlo);
   for (int t = tid; t < ND2; t += NT) s_D[t] = Dm.d[t];
   if (tid == 0) {
+    mbar_init(&s_bar, 1);
     const int t0 = int(atomicAdd(ticket, 1u));
     if (t0 == total_tickets - 1) atomicExch(ticket, 0u);
     s_tk[0] = t0;
-    if (t0 < nE) s_epoch = *reinterpret_cast<volatile unsigned*>(&flags[t0]);
+    if (t0 < nE) {
+      s_epoch = *reinterpret_cast<volatile unsigned*>(&flags[t0]);
+      mbar_expect_tx(&s_bar, GB);
+      bulk_g2s(s_g, geom + size_t(t0) * 6 * NLOC, GB, &s_bar);
+    }
   }
   __syncthreads();
   const unsigned target = s_epoch + 1u;  // every element's counter equals s_epoch at launch
-  int64_t prev = -1;
+  unsigned phase = 0;
+  int prev = -1;
   int buf = 0;
+  double pprev[ND];  // face-owned results of ticket t-1, summed once its neighbours are in
+#pragma unroll
+  for (int k = 0; k < ND; ++k) pprev[k] = 0.0;
 
-  auto coords = [&](int64_t el, int& ex, int& ey, int& ez) {
-    ex = int(el % sl.Ex);
-    ey = int((el / sl.Ex) % sl.Ey);
-    ez = sl.ez0 + int(el / LZ);
-  };
-  // owned node (i,j,k) of element (ex,ey,ez) has no contributor below it
-  auto finish_prev = [&](int64_t pe, const double* pout) {
-    int ex, ey, ez;
-    coords(pe, ex, ey, ez);
+  // owned node (i,j,k) of element pe that has a lower contributor: sum in ascending element id
+  auto finish_prev = [&](int pe) {
+    const int ex = pe % Ex, ey = (pe / Ex) % Ey, ez = sl.ez0 + pe / LZ;
     if (tid < 7) {  // wait for the <= 7 lower neighbours of pe (released long ago, normally)
       const int a = (tid + 1) & 1, b = ((tid + 1) >> 1) & 1, c = ((tid + 1) >> 2) & 1;
       if ((!a || ex > 0) && (!b || ey > 0) && (!c || ez > sl.ez0)) {
-        const int64_t nb = pe - a * LX - b * LY - c * LZ;
+        const int nb = pe - a - b * Ex - c * LZ;
         while (ld_relaxed(&flags[nb]) < target) {
         }
       }
     }
     __syncthreads();
     const bool hx = (i == 0 && ex > 0), hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
-    const bool ownx = (i < q) || (ex == sl.Ex - 1), owny = (j < q) || (ey == sl.Ey - 1);
+    const bool ownxy = ((i < q) || (ex == Ex - 1)) && ((j < q) || (ey == Ey - 1));
     const bool topz = (ez == sl.ez1 - 1);
-    const int64_t x = int64_t(ex) * q + i, y = int64_t(ey) * q + j, zb = int64_t(ez) * q;
-    const double* dbase = dep + pe * NLOC + ij;
-    const bool own0 = ownx && owny && hz;
-    const double cz = ldcg_pred(dbase - LZ * NLOC + q * ND2, own0);
-    const double cxz = ldcg_pred(dbase - (LZ + LX) * NLOC + q * ND2 + q, own0 && hx);
-    const double cyz = ldcg_pred(dbase - (LZ + LY) * NLOC + q * ND2 + q * ND, own0 && hy);
-    const double cxyz = ldcg_pred(dbase - (LZ + LY + LX) * NLOC + q * ND2 + q * ND + q, own0 && hx && hy);
+    const int x = ex * q + i, y = ey * q + j, zb = ez * q;
+    const int g0 = x + Nx * y + NxNy * (zb - zlo);
+    const bool mxy = sl.dirichlet && (x == 0 || x == Nx - 1 || y == 0 || y == Ny - 1);
+    const bool mz0 = sl.dirichlet && zb == 0, mzq = sl.dirichlet && zb + q == Nz - 1;
+    const double* dbase = dep + size_t(pe) * NLOC + ij;
+    const int oX = NLOC, oY = Ex * NLOC, oZ = LZ * NLOC;
+    const bool own0 = ownxy && hz;
+    const double cz = ldcg_pred(dbase - oZ + q * ND2, own0);
+    const double cxz = ldcg_pred(dbase - (oZ + oX) + q * ND2 + q, own0 && hx);
+    const double cyz = ldcg_pred(dbase - (oZ + oY) + q * ND2 + q * ND, own0 && hy);
+    const double cxyz = ldcg_pred(dbase - (oZ + oY + oX) + q * ND2 + q * ND + q, own0 && hx && hy);
     constexpr int KH = (ND + 1) / 2;
 #pragma unroll
     for (int kb = 0; kb < ND; kb += KH) {
@@ -475,15 +508,15 @@ __global__ void __launch_bounds__(ND* ND, SEMLAB_AXP_MINB)
 #pragma unroll
       for (int kk = 0; kk < KH; ++kk) {
         const int k = kb + kk;
-        const bool own = k < ND && ownx && owny && (k < q || topz);
-        cx[kk] = ldcg_pred(dbase - LX * NLOC + k * ND2 + q, own && hx);
-        cy[kk] = ldcg_pred(dbase - LY * NLOC + k * ND2 + q * ND, own && hy);
-        cxy[kk] = ldcg_pred(dbase - (LX + LY) * NLOC + k * ND2 + q * ND + q, own && hx && hy);
+        const bool own = k < ND && ownxy && (k < q || topz);
+        cx[kk] = ldcg_pred(dbase - oX + k * ND2 + q, own && hx);
+        cy[kk] = ldcg_pred(dbase - oY + k * ND2 + q * ND, own && hy);
+        cxy[kk] = ldcg_pred(dbase - (oX + oY) + k * ND2 + q * ND + q, own && hx && hy);
       }
 #pragma unroll
       for (int kk = 0; kk < KH; ++kk) {
         const int k = kb + kk;
-        if (k >= ND || !(ownx && owny && (k < q || topz))) continue;
+        if (k >= ND || !(ownxy && (k < q || topz))) continue;
         if (!(hx || hy || (k == 0 && hz))) continue;  // interior-owned: already written
         double acc = 0.0;
         if (k == 0) {  // (c=1): (b,a) = (1,1), (1,0), (0,1), (0,0)
@@ -495,38 +528,48 @@ __global__ void __launch_bounds__(ND* ND, SEMLAB_AXP_MINB)
         acc += cxy[kk];  // (c=0): (1,1), (1,0), (0,1), then the element itself
         acc += cy[kk];
         acc += cx[kk];
-        acc += pout[k * ND2 + ij];
-        const int64_t z = zb + k;
-        epi(sl.lidx(x, y, z), sl.masked(x, y, z) ? 0.0 : acc);
+        acc += pprev[k];
+        const bool m = mxy || (k == 0 && mz0) || (k == q && mzq);
+        epi(g0 + k * NxNy, m ? 0.0 : acc);
       }
     }
   };
 
   while (true) {
-    const int64_t el = s_tk[buf];
+    const int el = s_tk[buf];
     if (el >= nE) break;
     if (tid == 0) {  // next ticket now, so its latency hides behind this element
       const int tn = int(atomicAdd(ticket, 1u));
       if (tn == total_tickets - 1) atomicExch(ticket, 0u);
       s_tk[buf ^ 1] = tn;
     }
-    {  // this element's geometry -> L2
-      const char* gbase = reinterpret_cast<const char*>(geom + el * 6 * NLOC);
-      constexpr int lines = (6 * NLOC * int(sizeof(double)) + 127) / 128;
-      for (int l = tid; l < lines; l += NT) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + size_t(l) * 128));
-    }
-    int ex, ey, ez;
-    coords(el, ex, ey, ez);
-    const int64_t x = int64_t(ex) * q + i, y = int64_t(ey) * q + j, zb = int64_t(ez) * q;
+    const int ex = el % Ex, ey = (el / Ex) % Ey, ez = sl.ez0 + el / LZ;
+    const int x = ex * q + i, y = ey * q + j, zb = ez * q;
+    const int g0 = x + Nx * y + NxNy * (zb - zlo);
+    const bool mxy = sl.dirichlet && (x == 0 || x == Nx - 1 || y == 0 || y == Ny - 1);
+    const bool mz0 = sl.dirichlet && zb == 0, mzq = sl.dirichlet && zb + q == Nz - 1;
     double ureg[ND];
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
-      const double raw = __ldg(&u[sl.lidx(x, y, zb + k)]);
-      const double v = sl.masked(x, y, zb + k) ? 0.0 : raw;
+      const double raw = __ldg(u + g0 + k * NxNy);
+      const bool m = mxy || (k == 0 && mz0) || (k == q && mzq);
+      const double v = m ? 0.0 : raw;
       ureg[k] = v;
       s_a[k * ND2 + ij] = v;
     }
     __syncthreads();
+#if SEMLAB_AXP_UPREFETCH
+    {  // the next element's u rows (j', k') -> L2, one 64-byte row per thread
+      const int tn = s_tk[buf ^ 1];
+      if (tn < nE) {
+        const int nx = tn % Ex, ny = (tn / Ex) % Ey, nz = sl.ez0 + tn / LZ;
+        const int jj = tid % ND, kk = tid / ND;
+        const double* row = u + (nx * q) + Nx * (ny * q + jj) + NxNy * (nz * q + kk - zlo);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row + q));
+      }
+    }
+#endif
     double ur[ND], us[ND], ut[ND];
     {
       double Di[ND], Dj[ND];
@@ -549,34 +592,34 @@ __global__ void __launch_bounds__(ND* ND, SEMLAB_AXP_MINB)
         ut[k] = dt;
       }
     }
-    const double* gg = geom + el * 6 * NLOC + ij;
+    mbar_wait(&s_bar, phase);  // this element's geometry has landed in shared memory
+    phase ^= 1u;
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
-      const int node = k * ND2;
-      double g0, g1, g2, g3, g4, g5;
-      if (el >= 0) {  // always true: keeps per-layer load batches (bounded registers)
-        g0 = __ldcs(gg + 0 * NLOC + node);
-        g1 = __ldcs(gg + 1 * NLOC + node);
-        g2 = __ldcs(gg + 2 * NLOC + node);
-        g3 = __ldcs(gg + 3 * NLOC + node);
-        g4 = __ldcs(gg + 4 * NLOC + node);
-        g5 = __ldcs(gg + 5 * NLOC + node);
-      } else {
-        g0 = g1 = g2 = g3 = g4 = g5 = 0.0;
-      }
+      const GT* gk = s_g + k * ND2 + ij;
+      const double g0v = double(gk[0 * NLOC]), g1 = double(gk[1 * NLOC]), g2 = double(gk[2 * NLOC]);
+      const double g3 = double(gk[3 * NLOC]), g4 = double(gk[4 * NLOC]), g5 = double(gk[5 * NLOC]);
       const double r = ur[k], s = us[k], t = ut[k];
-      ur[k] = g0 * r + g1 * s + g2 * t;
+      ur[k] = g0v * r + g1 * s + g2 * t;
       us[k] = g1 * r + g3 * s + g4 * t;
       ut[k] = g2 * r + g4 * s + g5 * t;
     }
-    __syncthreads();
+    __syncthreads();  // s_g and s_a are free
+    if (tid == 0) {   // stream the next element's geometry while this one finishes
+      const int tn = s_tk[buf ^ 1];
+      if (tn < nE) {
+        fence_proxy_async_shared();
+        mbar_expect_tx(&s_bar, GB);
+        bulk_g2s(s_g, geom + size_t(tn) * 6 * NLOC, GB, &s_bar);
+      }
+    }
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       s_a[k * ND2 + ij] = ur[k];
       s_b[k * ND2 + ij] = us[k];
     }
     __syncthreads();
-    double* cur_out = s_out[buf];
+    double pcur[ND];
     {
       double DiT[ND], DjT[ND];
 #pragma unroll
@@ -584,7 +627,7 @@ __global__ void __launch_bounds__(ND* ND, SEMLAB_AXP_MINB)
         DiT[m] = s_D[m + ND * i];
         DjT[m] = s_D[m + ND * j];
       }
-      const bool ownx = (i < q) || (ex == sl.Ex - 1), owny = (j < q) || (ey == sl.Ey - 1);
+      const bool ownxy = ((i < q) || (ex == Ex - 1)) && ((j < q) || (ey == Ey - 1));
       const bool topz = (ez == sl.ez1 - 1);
       const bool hx = (i == 0 && ex > 0), hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
       double outk[ND];
@@ -600,49 +643,47 @@ __global__ void __launch_bounds__(ND* ND, SEMLAB_AXP_MINB)
         outk[k] = acc;
       }
       // owned nodes with no lower contributor are final now: batched epilogue (all vector
-      // loads first, then the stores); face-owned nodes wait in smem; the rest are deposited
+      // loads first, then the stores); face-owned nodes wait in registers; the rest are deposited
       typename EpiT::In in[ND];
-#if SEMLAB_AX_BATCH_EPI
 #pragma unroll
       for (int k = 0; k < ND; ++k) {
-        const bool own = ownx && owny && (k < q || topz);
-        if (own && !(hx || hy || (k == 0 && hz))) in[k] = epi.load(sl.lidx(x, y, zb + k));
+        const bool own = ownxy && (k < q || topz);
+        if (own && !(hx || hy || (k == 0 && hz))) in[k] = epi.load(g0 + k * NxNy);
       }
-#endif
+      double* dl = dep + size_t(el) * NLOC + ij;
 #pragma unroll
       for (int k = 0; k < ND; ++k) {
-        const bool own = ownx && owny && (k < q || topz);
+        const bool own = ownxy && (k < q || topz);
+        pcur[k] = outk[k];
         if (!own) {
-          dep[el * NLOC + k * ND2 + ij] = outk[k];
-        } else if (hx || hy || (k == 0 && hz)) {
-          cur_out[k * ND2 + ij] = outk[k];  // owned face node: summed once the neighbours are in
-        } else {
-          const int64_t z = zb + k;
-#if !SEMLAB_AX_BATCH_EPI
-          in[k] = epi.load(sl.lidx(x, y, z));
-#endif
-          epi.store(sl.lidx(x, y, z), in[k], sl.masked(x, y, z) ? 0.0 : outk[k]);
+          dl[k * ND2] = outk[k];
+        } else if (!(hx || hy || (k == 0 && hz))) {
+          const bool m = mxy || (k == 0 && mz0) || (k == q && mzq);
+          epi.store(g0 + k * NxNy, in[k], m ? 0.0 : outk[k]);
         }
       }
     }
     __syncthreads();
     if (tid == 0) st_release(&flags[el], target);
-    if (prev >= 0) finish_prev(prev, s_out[buf ^ 1]);
+    if (prev >= 0) finish_prev(prev);
+#pragma unroll
+    for (int k = 0; k < ND; ++k) pprev[k] = pcur[k];
     prev = el;
     buf ^= 1;
-    __syncthreads();
   }
-  if (prev >= 0) finish_prev(prev, s_out[buf ^ 1]);
+  if (prev >= 0) finish_prev(prev);
 }
 
-template <int ND, class EpiT>
-int64_t axp_launch(const Slab& sl, const double* u, const double* geom, const AxSync& sy, const EpiT& epi,
+template <int ND, class GT, class EpiT>
+int64_t axp_launch(const Slab& sl, const double* u, const GT* geom, const AxSync& sy, const EpiT& epi,
                    cudaStream_t s) {
   constexpr int NLOC = ND * ND * ND;
   const int64_t nE = sl.elems();
   if (nE == 0) return 0;
-  const size_t smem = (size_t(4) * NLOC + ND * ND) * sizeof(double);
-  auto kern = k_axp<ND, EpiT>;
+  if (sl.n_local() >= (int64_t(1) << 31) || nE * NLOC >= (int64_t(1) << 31))
+    invalid("SemSpace: a rank's lattice must have < 2^31 nodes");
+  const size_t smem = size_t(align128(geom_bytes<GT>(NLOC))) + (size_t(2) * NLOC + ND * ND) * sizeof(double);
+  auto kern = k_axp<ND, EpiT, GT>;
   static int nctas = 0;  // resident CTAs: occupancy x SMs (per instantiation)
   if (nctas == 0) {
     SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -658,10 +699,377 @@ int64_t axp_launch(const Slab& sl, const double* u, const double* geom, const Ax
   return 1;
 }
 
+// ------------------------------------------------------------------------ warp-per-element Ax (p = 7)
+// The p=7 operator on the FP64 tensor cores. Every contraction of sem_space.cpp:137-174 is a
+// stack of 8x8x8 products, i.e. two mma.m8n8k4.f64 (DMMA) each:
+//   ur_k = U_k D^T, us_k = D U_k (per z-layer k), ut_(.,j,.) = D U_(.,j,.) (per y-row j),
+//   out_k = Gr_k D + D^T Gs_k (+) D^T Gt_(.,j,.)
+// so an element costs 96 DMMA instead of 2 x 384 DFMA warp-instructions, and the kernel is no
+// longer issue-bound. One warp owns one element at a time (no CTA barriers: __syncwarp only);
+// the warp loops over dynamic tickets in ascending element id and implements Q^T with the same
+// owner protocol and summation order as k_ax/k_axp (deposits, per-element release counters,
+// face-owned nodes finished one ticket later). A lane holds the nodes (k = 0..7, j = lane/4,
+// i = 2(lane%4) + {0,1}), the D-fragments live in 4 registers, and the per-warp shared
+// workspace (3 arrays of 8 z-layers) is padded and XOR-swizzled so every fragment access is
+// conflict-free (2 wavefronts per 256 B).
+namespace axw {
+constexpr int PS = 72;  // z-layer stride (doubles): 64 + 8 so consecutive layers use opposite bank halves
+constexpr int ARR = 8 * PS;
+__device__ __forceinline__ int sidx(int k, int j, int i) {  // swizzled workspace index
+  return k * PS + j * 8 + 2 * ((i >> 1) ^ ((j >> 1) & 3)) + (i & 1);
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+}  // namespace axw
+
+#ifndef SEMLAB_AXW_WARPS
+#define SEMLAB_AXW_WARPS 4  // warps (independent element pipelines) per CTA
+#endif
+#ifndef SEMLAB_AXW_GPF
+#define SEMLAB_AXW_GPF 2  // geometry L2 prefetch: 0 none, 1 one element ahead, 2 current element, 3 bulk (current)
+#endif
+#ifndef SEMLAB_AXW_MINB
+#define SEMLAB_AXW_MINB 3  // resident CTAs per SM (register cap 168)
+#endif
+
+template <class EpiT>
+__global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
+    k_axw(const Slab sl, const DMat<8> Dm, const double* __restrict__ u, const double* __restrict__ geom,
+          double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int total_tickets,
+          const EpiT epi) {
+  using namespace axw;
+  constexpr int ND = 8, ND2 = 64, NLOC = 512, q = 7;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* sU = reinterpret_cast<double*>(smem_raw) + size_t(wid) * 3 * ARR;  // u, then Gr
+  double* sS = sU + ARR;                                                      // Gs
+  double* sT = sS + ARR;                                                      // ut, Gt, then D^T Gt
+  const int gj = lane >> 2, gc = lane & 3;  // fragment row / column group
+  const int j = gj, i0 = 2 * gc;            // this lane's nodes: (k, j, i0 + {0,1})
+  // D fragments: Df[kc] = D(lane/4, lane%4 + 4kc), Dt[kc] = D(lane%4 + 4kc, lane/4)
+  double Df[2], Dt[2];
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc) {
+    Df[kc] = Dm.d[gj + ND * (gc + 4 * kc)];
+    Dt[kc] = Dm.d[(gc + 4 * kc) + ND * gj];
+  }
+  const int nE = int(sl.elems());
+  const int Ex = sl.Ex, Ey = sl.Ey, LZ = Ex * Ey;
+  const int Nx = int(sl.Nx), Ny = int(sl.Ny), Nz = int(sl.Nz), NxNy = Nx * Ny;
+  const int zlo = int(sl.zlo);
+
+  auto take = [&]() {
+    int t = 0;
+    if (lane == 0) {
+      t = int(atomicAdd(ticket, 1u));
+      if (t == total_tickets - 1) atomicExch(ticket, 0u);
+    }
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+  auto prefetch_geom = [&](int e) {  // element e's geometry (24 KB) -> L2
+    const char* gb = reinterpret_cast<const char*>(geom + size_t(e) * 6 * NLOC);
+    if (SEMLAB_AXW_GPF == 3) {  // one bulk (TMA engine) L2 prefetch
+      if (lane == 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gb), "r"(6 * NLOC * 8) : "memory");
+    } else {
+#pragma unroll
+      for (int l = 0; l < 6; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(gb + (l * 32 + lane) * 128));
+    }
+  };
+  auto prefetch = [&](int e) {  // element e's u rows (and geometry, SEMLAB_AXW_GPF=1) -> L2
+    if (e >= nE) return;
+    if (SEMLAB_AXW_GPF == 1) prefetch_geom(e);
+    const int ex = e % Ex, ey = (e / Ex) % Ey, ez = sl.ez0 + e / LZ;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = lane * 2 + r, jj = row & 7, kk = row >> 3;
+      const double* p = u + (ex * q) + Nx * (ey * q + jj) + NxNy * (ez * q + kk - zlo);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p + q));
+    }
+  };
+
+  int el = take();
+  if (el >= nE) return;
+  const unsigned target = *reinterpret_cast<volatile unsigned*>(&flags[el]) + 1u;
+  int prev = -1;
+  double pprev[16];  // face-owned results of ticket t-1 ([k][i - i0])
+#pragma unroll
+  for (int t = 0; t < 16; ++t) pprev[t] = 0.0;
+
+  auto finish_prev = [&](int pe) {
+    const int ex = pe % Ex, ey = (pe / Ex) % Ey, ez = sl.ez0 + pe / LZ;
+    if (lane < 7) {  // wait for the <= 7 lower neighbours of pe (released long ago, normally)
+      const int a = (lane + 1) & 1, b = ((lane + 1) >> 1) & 1, c = ((lane + 1) >> 2) & 1;
+      if ((!a || ex > 0) && (!b || ey > 0) && (!c || ez > sl.ez0)) {
+        const int nb = pe - a - b * Ex - c * LZ;
+        while (ld_relaxed(&flags[nb]) < target) {
+        }
+      }
+    }
+    __syncwarp();
+    const bool hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
+    const bool owny = (j < q) || (ey == Ey - 1);
+    const bool topz = (ez == sl.ez1 - 1);
+    const int y = ey * q + j, zb = ez * q;
+    const bool mz0 = sl.dirichlet && zb == 0, mzq = sl.dirichlet && zb + q == Nz - 1;
+    const bool my = sl.dirichlet && (y == 0 || y == Ny - 1);
+    const double* db = dep + size_t(pe) * NLOC + j * ND;
+    const int oX = NLOC, oY = Ex * NLOC, oZ = LZ * NLOC;
+    // all predicated deposit loads of a 4-layer batch for both of this lane's columns are in
+    // flight together (two L2 round trips per element)
+    const int x0 = ex * q + i0;
+    const bool hx0 = (i0 == 0 && ex > 0);
+    const bool ownx1 = (i0 + 1 < q) || (ex == Ex - 1);
+    const int g0 = x0 + Nx * y + NxNy * (zb - zlo);
+    const bool mx[2] = {my || (sl.dirichlet && (x0 == 0 || x0 == Nx - 1)), my || (sl.dirichlet && (x0 + 1 == Nx - 1))};
+    const bool ownxy[2] = {owny, ownx1 && owny};  // i0 is even, so i0 < q
+    const bool hx[2] = {hx0, false};
+    const double* d = db + i0;
+    double cz[2], cxz[2], cyz[2], cxyz[2];
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii) {
+      const bool own0 = ownxy[ii] && hz;
+      cxyz[ii] = ldcg_pred(d + ii - (oZ + oY + oX) + q * ND2 + q * ND + q, own0 && hx[ii] && hy);
+      cyz[ii] = ldcg_pred(d + ii - (oZ + oY) + q * ND2 + q * ND, own0 && hy);
+      cxz[ii] = ldcg_pred(d + ii - (oZ + oX) + q * ND2 + q, own0 && hx[ii]);
+      cz[ii] = ldcg_pred(d + ii - oZ + q * ND2, own0);
+    }
+#pragma unroll
+    for (int kb = 0; kb < ND; kb += 4) {
+      double cx[4][2], cy[4][2], cxy[4][2];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = kb + kk;
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii) {
+          const bool own = ownxy[ii] && (k < q || topz);
+          cxy[kk][ii] = ldcg_pred(d + ii - (oX + oY) + k * ND2 + q * ND + q, own && hx[ii] && hy);
+          cy[kk][ii] = ldcg_pred(d + ii - oY + k * ND2 + q * ND, own && hy);
+          cx[kk][ii] = ldcg_pred(d + ii - oX + k * ND2 + q, own && hx[ii]);
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = kb + kk;
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii) {
+          if (!(ownxy[ii] && (k < q || topz))) continue;
+          if (!(hx[ii] || hy || (k == 0 && hz))) continue;  // interior-owned: already written
+          double acc = 0.0;
+          if (k == 0) {  // (c=1): (b,a) = (1,1), (1,0), (0,1), (0,0)
+            acc += cxyz[ii];
+            acc += cyz[ii];
+            acc += cxz[ii];
+            acc += cz[ii];
+          }
+          acc += cxy[kk][ii];  // (c=0): (1,1), (1,0), (0,1), then the element itself
+          acc += cy[kk][ii];
+          acc += cx[kk][ii];
+          acc += pprev[k * 2 + ii];
+          const bool m = mx[ii] || (k == 0 && mz0) || (k == q && mzq);
+          epi(g0 + k * NxNy + ii, m ? 0.0 : acc);
+        }
+      }
+    }
+  };
+
+  int nxt = take();
+  while (true) {
+    if (SEMLAB_AXW_GPF >= 2) prefetch_geom(el);
+    prefetch(nxt);
+    const int ex = el % Ex, ey = (el / Ex) % Ey, ez = sl.ez0 + el / LZ;
+    const int y = ey * q + j, zb = ez * q;
+    const int xb = ex * q + i0;
+    const int g0 = xb + Nx * y + NxNy * (zb - zlo);
+    const bool my = sl.dirichlet && (y == 0 || y == Ny - 1);
+    const bool mx0 = my || (sl.dirichlet && (xb == 0 || xb == Nx - 1));
+    const bool mx1 = my || (sl.dirichlet && (xb + 1 == Nx - 1));
+    const bool mz0 = sl.dirichlet && zb == 0, mzq = sl.dirichlet && zb + q == Nz - 1;
+    // u: this lane's 16 nodes -> swizzled workspace
+    {
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < ND; ++k) {
+        v[2 * k] = __ldg(u + g0 + k * NxNy);
+        v[2 * k + 1] = __ldg(u + g0 + k * NxNy + 1);
+      }
+#pragma unroll
+      for (int k = 0; k < ND; ++k) {
+        const bool mz = (k == 0 && mz0) || (k == q && mzq);
+        const double a = (mx0 || mz) ? 0.0 : v[2 * k], b = (mx1 || mz) ? 0.0 : v[2 * k + 1];
+        *reinterpret_cast<double2*>(sU + sidx(k, j, i0)) = make_double2(a, b);
+      }
+    }
+    __syncwarp();  // also orders every lane's deposits of ticket t-1 before lane 0's release
+    if (prev >= 0 && lane == 0) st_release(&flags[prev], target);
+    // ut: per y-row jj, (k, i) <- D (k, m) U(m, jj, i)
+#pragma unroll
+    for (int jj = 0; jj < ND; ++jj) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) dmma(c0, c1, Df[kc], sU[sidx(gc + 4 * kc, jj, gj)]);
+      *reinterpret_cast<double2*>(sT + sidx(gj, jj, i0)) = make_double2(c0, c1);
+    }
+    __syncwarp();
+    // per z-layer: ur, us (DMMA), ut (workspace), geometric factors, then Gr/Gs/Gt back out
+    const double* ge = geom + size_t(el) * 6 * NLOC + j * ND + i0;
+    double2 gA[6], gB[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) gA[c] = __ldcs(reinterpret_cast<const double2*>(ge + c * NLOC));
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      double2* gcur = (k & 1) ? gB : gA;
+      double2* gnext = (k & 1) ? gA : gB;
+      if (k + 1 < ND) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          gnext[c] = __ldcs(reinterpret_cast<const double2*>(ge + c * NLOC + (k + 1) * ND2));
+      }
+      double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) {
+        dmma(r0, r1, sU[sidx(k, gj, gc + 4 * kc)], Df[kc]);
+        dmma(s0, s1, Df[kc], sU[sidx(k, gc + 4 * kc, gj)]);
+      }
+      const double2 t2 = *reinterpret_cast<const double2*>(sT + sidx(k, j, i0));
+      __syncwarp();  // every lane has read layer k of u before it is overwritten by Gr
+      double gr[2], gs[2], gt[2];
+      {
+        const double rr[2] = {r0, r1}, ss[2] = {s0, s1}, tt[2] = {t2.x, t2.y};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double G0 = h ? gcur[0].y : gcur[0].x, G1 = h ? gcur[1].y : gcur[1].x;
+          const double G2 = h ? gcur[2].y : gcur[2].x, G3 = h ? gcur[3].y : gcur[3].x;
+          const double G4 = h ? gcur[4].y : gcur[4].x, G5 = h ? gcur[5].y : gcur[5].x;
+          gr[h] = G0 * rr[h] + G1 * ss[h] + G2 * tt[h];
+          gs[h] = G1 * rr[h] + G3 * ss[h] + G4 * tt[h];
+          gt[h] = G2 * rr[h] + G4 * ss[h] + G5 * tt[h];
+        }
+      }
+      *reinterpret_cast<double2*>(sU + sidx(k, j, i0)) = make_double2(gr[0], gr[1]);
+      *reinterpret_cast<double2*>(sS + sidx(k, j, i0)) = make_double2(gs[0], gs[1]);
+      *reinterpret_cast<double2*>(sT + sidx(k, j, i0)) = make_double2(gt[0], gt[1]);
+    }
+    __syncwarp();
+    // out_k = Gr_k D + D^T Gs_k
+    double o[16];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) dmma(c0, c1, sU[sidx(k, gj, gc + 4 * kc)], Dt[kc]);
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) dmma(c0, c1, Dt[kc], sS[sidx(k, gc + 4 * kc, gj)]);
+      o[2 * k] = c0;
+      o[2 * k + 1] = c1;
+    }
+    // + D^T Gt per y-row (in place in the workspace: row jj is read and written only here)
+#pragma unroll
+    for (int jj = 0; jj < ND; ++jj) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) dmma(c0, c1, Dt[kc], sT[sidx(gc + 4 * kc, jj, gj)]);
+      __syncwarp();
+      *reinterpret_cast<double2*>(sT + sidx(gj, jj, i0)) = make_double2(c0, c1);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const double2 t2 = *reinterpret_cast<const double2*>(sT + sidx(k, j, i0));
+      o[2 * k] += t2.x;
+      o[2 * k + 1] += t2.y;
+    }
+    // epilogue: deposit non-owned, finish interior-owned now, keep face-owned in registers
+    {
+      const bool owny = (j < q) || (ey == Ey - 1);
+      const bool topz = (ez == sl.ez1 - 1);
+      const bool hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
+      double* dl = dep + size_t(el) * NLOC + j * ND + i0;
+#pragma unroll
+      for (int kb = 0; kb < ND; kb += 4) {
+        typename EpiT::In in[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int k = kb + t / 2, ii = t % 2, i = i0 + ii;
+          const bool own = ((i < q) || (ex == Ex - 1)) && owny && (k < q || topz);
+          const bool hx = (i == 0 && ex > 0);
+          if (own && !(hx || hy || (k == 0 && hz))) in[t] = epi.load(g0 + k * NxNy + ii);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int k = kb + t / 2, ii = t % 2, i = i0 + ii;
+          const bool own = ((i < q) || (ex == Ex - 1)) && owny && (k < q || topz);
+          const bool hx = (i == 0 && ex > 0);
+          const double v = o[2 * k + ii];
+          if (!own) {
+            dl[k * ND2 + ii] = v;
+          } else if (!(hx || hy || (k == 0 && hz))) {
+            const bool m = (ii ? mx1 : mx0) || (k == 0 && mz0) || (k == q && mzq);
+            epi.store(g0 + k * NxNy + ii, in[t], m ? 0.0 : v);
+          }
+        }
+      }
+    }
+    // the release of this element is deferred until the next element's u has been gathered
+    // (its MEMBAR then finds the deposits long acknowledged instead of stalling the warp)
+    if (prev >= 0) finish_prev(prev);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) pprev[t] = o[t];
+    prev = el;
+    el = nxt;
+    if (el >= nE) break;
+    nxt = take();
+  }
+  __syncwarp();
+  if (lane == 0) st_release(&flags[prev], target);
+  finish_prev(prev);
+}
+
+template <class EpiT>
+int64_t axw_launch(const Slab& sl, const double* u, const double* geom, const AxSync& sy, const EpiT& epi,
+                   cudaStream_t s) {
+  constexpr int NLOC = 512;
+  const int64_t nE = sl.elems();
+  if (nE == 0) return 0;
+  if (sl.n_local() >= (int64_t(1) << 31) || nE * NLOC >= (int64_t(1) << 31))
+    invalid("SemSpace: a rank's lattice must have < 2^31 nodes");
+  constexpr int W = SEMLAB_AXW_WARPS;
+  const size_t smem = size_t(W) * 3 * axw::ARR * sizeof(double);
+  auto kern = k_axw<EpiT>;
+  static int nctas = 0;
+  if (nctas == 0) {
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0, dev = 0, sms = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem));
+    SB_CUDA(cudaGetDevice(&dev));
+    SB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    nctas = std::max(1, per_sm * sms);
+  }
+  const int grid = int(std::min<int64_t>(nctas, (nE + W - 1) / W));
+  kern<<<grid, 32 * W, smem, s>>>(sl, dmat<8>(sl.q), u, geom, sy.dep, sy.flags, sy.ticket, int(nE + int64_t(grid) * W),
+                                   epi);
+  SB_LAUNCH_CHECK();
+  return 1;
+}
+
+bool ax_dmma() {  // SEMLAB_AX_DMMA=0 selects the FP64-FMA persistent kernel (A/B measurement)
+  static const bool on = [] {
+    const char* e = std::getenv("SEMLAB_AX_DMMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int ND, bool LOCAL, class EpiT>
 int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, const AxSync& sy, double* out_local,
                        const EpiT& epi, cudaStream_t s) {
   if constexpr (!LOCAL && ND >= 8) {
+    if constexpr (ND == 8) {
+      if (ax_dmma()) return axw_launch(sl, u, geom, sy, epi, s);
+    }
     if (ax_persistent()) return axp_launch<ND>(sl, u, geom, sy, epi, s);
   }
   constexpr int EPB = epb<ND>();
