@@ -731,6 +731,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SEMLAB_AXW_GPF
 #define SEMLAB_AXW_GPF 2  // geometry L2 prefetch: 0 none, 1 one element ahead, 2 current element, 3 bulk (current)
 #endif
+#ifndef SEMLAB_AXW_PDEP
+#define SEMLAB_AXW_PDEP 1  // face-owned results wait in the element's deposit slots, not registers
+#endif
 #ifndef SEMLAB_AXW_MINB
 #define SEMLAB_AXW_MINB 3  // resident CTAs per SM (register cap 168)
 #endif
@@ -795,9 +798,11 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
   if (el >= nE) return;
   const unsigned target = *reinterpret_cast<volatile unsigned*>(&flags[el]) + 1u;
   int prev = -1;
+#if !SEMLAB_AXW_PDEP
   double pprev[16];  // face-owned results of ticket t-1 ([k][i - i0])
 #pragma unroll
   for (int t = 0; t < 16; ++t) pprev[t] = 0.0;
+#endif
 
   auto finish_prev = [&](int pe) {
     const int ex = pe % Ex, ey = (pe / Ex) % Ey, ez = sl.ez0 + pe / LZ;
@@ -840,6 +845,9 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
 #pragma unroll
     for (int kb = 0; kb < ND; kb += 4) {
       double cx[4][2], cy[4][2], cxy[4][2];
+#if SEMLAB_AXW_PDEP
+      double cs[4][2];  // the element's own face-owned results, parked in its deposit slots
+#endif
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const int k = kb + kk;
@@ -849,6 +857,9 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
           cxy[kk][ii] = ldcg_pred(d + ii - (oX + oY) + k * ND2 + q * ND + q, own && hx[ii] && hy);
           cy[kk][ii] = ldcg_pred(d + ii - oY + k * ND2 + q * ND, own && hy);
           cx[kk][ii] = ldcg_pred(d + ii - oX + k * ND2 + q, own && hx[ii]);
+#if SEMLAB_AXW_PDEP
+          cs[kk][ii] = ldcg_pred(d + ii + k * ND2, own && (hx[ii] || hy || (k == 0 && hz)));
+#endif
         }
       }
 #pragma unroll
@@ -868,7 +879,11 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
           acc += cxy[kk][ii];  // (c=0): (1,1), (1,0), (0,1), then the element itself
           acc += cy[kk][ii];
           acc += cx[kk][ii];
+#if SEMLAB_AXW_PDEP
+          acc += cs[kk][ii];
+#else
           acc += pprev[k * 2 + ii];
+#endif
           const bool m = mx[ii] || (k == 0 && mz0) || (k == q && mzq);
           epi(g0 + k * NxNy + ii, m ? 0.0 : acc);
         }
@@ -1004,8 +1019,8 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
           const bool own = ((i < q) || (ex == Ex - 1)) && owny && (k < q || topz);
           const bool hx = (i == 0 && ex > 0);
           const double v = o[2 * k + ii];
-          if (!own) {
-            dl[k * ND2 + ii] = v;
+          if (!own || (SEMLAB_AXW_PDEP && (hx || hy || (k == 0 && hz)))) {
+            dl[k * ND2 + ii] = v;  // deposit (or, face-owned, park until the neighbours are in)
           } else if (!(hx || hy || (k == 0 && hz))) {
             const bool m = (ii ? mx1 : mx0) || (k == 0 && mz0) || (k == q && mzq);
             epi.store(g0 + k * NxNy + ii, in[t], m ? 0.0 : v);
@@ -1016,8 +1031,10 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
     // the release of this element is deferred until the next element's u has been gathered
     // (its MEMBAR then finds the deposits long acknowledged instead of stalling the warp)
     if (prev >= 0) finish_prev(prev);
+#if !SEMLAB_AXW_PDEP
 #pragma unroll
     for (int t = 0; t < 16; ++t) pprev[t] = o[t];
+#endif
     prev = el;
     el = nxt;
     if (el >= nE) break;
