@@ -738,9 +738,17 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #define SEMLAB_AXW_MINB 3  // resident CTAs per SM (register cap 168)
 #endif
 
-template <class EpiT>
+__device__ __forceinline__ double2 ld_geom2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld_geom2(const float* p) {
+  const float2 v = __ldcs(reinterpret_cast<const float2*>(p));
+  return make_double2(double(v.x), double(v.y));
+}
+
+// GT = double: the operator itself (Krylov A). GT = float: the smoother's operator with the
+// geometric factors rounded to FP32 (half the bytes; arithmetic stays FP64 on the DMMA path).
+template <class EpiT, class GT>
 __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
-    k_axw(const Slab sl, const DMat<8> Dm, const double* __restrict__ u, const double* __restrict__ geom,
+    k_axw(const Slab sl, const DMat<8> Dm, const double* __restrict__ u, const GT* __restrict__ geom,
           double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int total_tickets,
           const EpiT epi) {
   using namespace axw;
@@ -772,13 +780,15 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
     }
     return __shfl_sync(0xffffffffu, t, 0);
   };
-  auto prefetch_geom = [&](int e) {  // element e's geometry (24 KB) -> L2
+  auto prefetch_geom = [&](int e) {  // element e's geometry (24 KB FP64 / 12 KB FP32) -> L2
     const char* gb = reinterpret_cast<const char*>(geom + size_t(e) * 6 * NLOC);
+    constexpr int GL = 6 * NLOC * int(sizeof(GT)) / 128 / 32;  // 128-byte lines per lane
     if (SEMLAB_AXW_GPF == 3) {  // one bulk (TMA engine) L2 prefetch
-      if (lane == 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gb), "r"(6 * NLOC * 8) : "memory");
+      if (lane == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gb), "r"(6 * NLOC * int(sizeof(GT))) : "memory");
     } else {
 #pragma unroll
-      for (int l = 0; l < 6; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(gb + (l * 32 + lane) * 128));
+      for (int l = 0; l < GL; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(gb + (l * 32 + lane) * 128));
     }
   };
   auto prefetch = [&](int e) {  // element e's u rows (and geometry, SEMLAB_AXW_GPF=1) -> L2
@@ -930,10 +940,10 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
     }
     __syncwarp();
     // per z-layer: ur, us (DMMA), ut (workspace), geometric factors, then Gr/Gs/Gt back out
-    const double* ge = geom + size_t(el) * 6 * NLOC + j * ND + i0;
+    const GT* ge = geom + size_t(el) * 6 * NLOC + j * ND + i0;
     double2 gA[6], gB[6];
 #pragma unroll
-    for (int c = 0; c < 6; ++c) gA[c] = __ldcs(reinterpret_cast<const double2*>(ge + c * NLOC));
+    for (int c = 0; c < 6; ++c) gA[c] = ld_geom2(ge + c * NLOC);
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       double2* gcur = (k & 1) ? gB : gA;
@@ -941,7 +951,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
       if (k + 1 < ND) {
 #pragma unroll
         for (int c = 0; c < 6; ++c)
-          gnext[c] = __ldcs(reinterpret_cast<const double2*>(ge + c * NLOC + (k + 1) * ND2));
+          gnext[c] = ld_geom2(ge + c * NLOC + (k + 1) * ND2);
       }
       double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -1045,8 +1055,8 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
   finish_prev(prev);
 }
 
-template <class EpiT>
-int64_t axw_launch(const Slab& sl, const double* u, const double* geom, const AxSync& sy, const EpiT& epi,
+template <class EpiT, class GT>
+int64_t axw_launch(const Slab& sl, const double* u, const GT* geom, const AxSync& sy, const EpiT& epi,
                    cudaStream_t s) {
   constexpr int NLOC = 512;
   const int64_t nE = sl.elems();
@@ -1055,7 +1065,7 @@ int64_t axw_launch(const Slab& sl, const double* u, const double* geom, const Ax
     invalid("SemSpace: a rank's lattice must have < 2^31 nodes");
   constexpr int W = SEMLAB_AXW_WARPS;
   const size_t smem = size_t(W) * 3 * axw::ARR * sizeof(double);
-  auto kern = k_axw<EpiT>;
+  auto kern = k_axw<EpiT, GT>;
   static int nctas = 0;
   if (nctas == 0) {
     SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1341,6 +1351,19 @@ int64_t launch_ax(const Slab& sl, const double* u, const double* geom, const AxS
   return 0;
 }
 
+int64_t launch_ax_g32(const Slab& sl, const double* u, const float* geom32, const AxSync& sy, Epi epi,
+                      const EpiArgs& a, cudaStream_t s) {
+  if (sl.q != 7) invalid("launch_ax_g32: FP32 geometry is implemented for order 7");
+  switch (epi) {
+    case Epi::Write: return axw_launch(sl, u, geom32, sy, EWrite{a.w}, s);
+    case Epi::Residual: return axw_launch(sl, u, geom32, sy, EResidual{a.w, a.b}, s);
+    case Epi::ChebJacStep:
+      return axw_launch(sl, u, geom32, sy, EChebJacStep{a.x, a.r, a.d, a.inv, a.c1, a.c2}, s);
+    case Epi::ChebJacInit: return axw_launch(sl, u, geom32, sy, EChebJacInit{a.r, a.d, a.b, a.inv, a.c1}, s);
+  }
+  return 0;
+}
+
 int64_t launch_ax_local(const Slab& sl, const double* uloc, const double* geom, double* out, cudaStream_t s) {
   return ax_dispatch<true>(sl, uloc, geom, AxSync{}, out, EWrite{nullptr}, s);
 }
@@ -1397,6 +1420,10 @@ int64_t launch_copy(double* dst, const double* src, int64_t n, cudaStream_t s) {
   if (n > 0) SB_CUDA(cudaMemcpyAsync(dst, src, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
   return 0;
 }
+int64_t launch_to_f32(const double* in, float* out, int64_t n, cudaStream_t s) {
+  return foreach(n, s, [=] __device__(int64_t t) { out[t] = float(in[t]); });
+}
+
 int64_t launch_axpby(double* y, double a, const double* x, double b, int64_t n, cudaStream_t s) {
   return foreach(n, s, [=] __device__(int64_t t) { y[t] = a * x[t] + b * y[t]; });
 }

@@ -37,6 +37,10 @@ int64_t launch_geom(const Slab& sl, const double* d_X, double* d_geom, double* d
                     unsigned long long* d_bad, cudaStream_t s);
 int64_t launch_ax(const Slab& sl, const double* d_u, const double* d_geom, const AxSync& sync, Epi epi,
                   const EpiArgs& a, cudaStream_t s);
+// Same operator with FP32-rounded geometric factors (order 7 only): the smoother's A.
+int64_t launch_ax_g32(const Slab& sl, const double* d_u, const float* d_geom32, const AxSync& sync, Epi epi,
+                      const EpiArgs& a, cudaStream_t s);
+int64_t launch_to_f32(const double* in, float* out, int64_t n, cudaStream_t s);
 int64_t launch_ax_local(const Slab& sl, const double* d_uloc, const double* d_geom, double* d_out,
                         cudaStream_t s);
 int64_t launch_local_diag(const Slab& sl, const double* d_geom, double* d_out_local, cudaStream_t s);

@@ -56,6 +56,7 @@ struct semlab_space_s {
   std::vector<double> coords;  // host lattice coords of the local planes (3 per point)
   sb::DevBuf<double> geom, massw, mass_diag, inv_diag, dep, scratch_e, plane_lo, plane_hi;
   sb::DevBuf<unsigned> flags, ticket;
+  sb::DevBuf<float> geom32;  // FP32-rounded geometric factors (the smoother's operator, order 7)
   bool has_inv_diag = false;
   bool full = false;  // whole mesh on this rank even under a distributed context (coarse solve)
   bool distributed() const { return !full && ctx->nranks > 1; }
@@ -64,9 +65,12 @@ struct semlab_space_s {
 
   void build();
   sb::AxSync sync() const { return {dep.p, flags.p, ticket.p}; }
-  // A with an epilogue; handles the slab interface sum when distributed.
-  void apply_A(const double* in, double* out);
-  void ax(const double* in, sb::Epi epi, const sb::EpiArgs& a);
+  // A with an epilogue; handles the slab interface sum when distributed. g32: use the
+  // FP32-rounded geometric factors (only where has_geom32()).
+  void apply_A(const double* in, double* out, bool g32 = false);
+  void ax(const double* in, sb::Epi epi, const sb::EpiArgs& a, bool g32 = false);
+  bool enable_geom32();  // builds geom32 if the order supports it; false otherwise
+  bool has_geom32() const { return geom32.p != nullptr; }
   const double* jacobi_inv();
   void stiffness_diag(double* out);
   int64_t own_off() const { return sl.lidx(0, 0, sl.own_z0()); }
@@ -88,6 +92,7 @@ struct semlab_op_s {
   semlab_pmg_s* pmg = nullptr;
   semlab_apply_fn fn = nullptr;
   void* user = nullptr;
+  bool geom32 = false;  // kA: apply with the FP32-rounded geometric factors (smoother operator)
   void apply(const double* in, double* out);
 };
 

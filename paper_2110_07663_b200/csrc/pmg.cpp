@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 
@@ -434,6 +435,15 @@ semlab_pmg_s::~semlab_pmg_s() {
   delete coarse_full;
 }
 
+// SEMLAB_SMOOTHER_GEOM32=0 keeps FP64 geometric factors in the FP32 smoother (A/B measurement).
+static bool smoother_geom32() {
+  static const bool on = [] {
+    const char* e = std::getenv("SEMLAB_SMOOTHER_GEOM32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void semlab_pmg_s::build() {
   const size_t nl = orders.size();
   if (nl < 2) invalid("pmg: schedule needs at least two levels");
@@ -463,6 +473,9 @@ void semlab_pmg_s::build() {
     L.A->ctx = ctx;
     L.A->n = n;
     L.A->space = L.sp;
+    // FP32 smoother (the paper's setting): its operator applications use FP32-rounded
+    // geometric factors too (FP64 arithmetic); the Krylov operator keeps the FP64 factors.
+    if (precision == 32 && smoother_geom32()) L.A->geom32 = L.sp->enable_geom32();
     L.S = new semlab_op_s;
     L.S->ctx = ctx;
     L.S->n = n;
@@ -573,13 +586,13 @@ void semlab_pmg_s::cycle(int l) {
   SB_CUDA(cudaMemsetAsync(L.x.p, 0, size_t(n) * sizeof(double), s));
   L.cheb->smooth(L.b.p, L.x.p, true);
   if (L.sp->distributed()) {  // the residual needs the summed interface planes first
-    L.sp->apply_A(L.x.p, L.r.p);
+    L.sp->apply_A(L.x.p, L.r.p, L.A->geom32);
     ctx->count(launch_sub(L.r.p, L.b.p, L.r.p, n, s));
   } else {
     EpiArgs a;
     a.w = L.r.p;
     a.b = L.b.p;
-    L.sp->ax(L.x.p, Epi::Residual, a);
+    L.sp->ax(L.x.p, Epi::Residual, a, L.A->geom32);
   }
   restrict_(l, L.r.p, lv[size_t(l) + 1].b.p);
   cycle(l + 1);

@@ -73,7 +73,7 @@ void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
       a.b = b;
       a.inv = inv;
       a.c1 = theta;
-      sp->ax(x, Epi::ChebJacInit, a);
+      sp->ax(x, Epi::ChebJacInit, a, A->geom32);
     }
     double rho = 1.0 / sigma;
     for (int k = 1; k <= params.order; ++k) {
@@ -85,7 +85,7 @@ void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
       a.inv = inv;
       a.c1 = rho_next * rho;
       a.c2 = 2.0 * rho_next / delta;
-      sp->ax(d.p, Epi::ChebJacStep, a);
+      sp->ax(d.p, Epi::ChebJacStep, a, A->geom32);
       rho = rho_next;
     }
     ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));
@@ -106,7 +106,7 @@ void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
       EpiArgs a;
       a.w = t.p;
       a.b = b;
-      sp->ax(x, Epi::Residual, a);
+      sp->ax(x, Epi::Residual, a, A->geom32);
       sch->ras(t.p, 1, e);
     }
     double rho = 1.0 / sigma;
@@ -114,7 +114,7 @@ void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
       const double rho_next = 1.0 / (2.0 * sigma - rho);
       EpiArgs a;
       a.w = t.p;
-      sp->ax(d.p, Epi::Write, a);
+      sp->ax(d.p, Epi::Write, a, A->geom32);
       RasEpi es;
       es.x = x;
       es.r = r.p;

@@ -184,15 +184,27 @@ void semlab_space_s::owner_copy_up(double* v) {
   SB_NCCL(ncclGroupEnd());
 }
 
-void semlab_space_s::ax(const double* in, Epi epi, const EpiArgs& a) {
-  ctx->count(launch_ax(sl, in, geom.p, sync(), epi, a, ctx->stream));
+void semlab_space_s::ax(const double* in, Epi epi, const EpiArgs& a, bool g32) {
+  if (g32 && has_geom32())
+    ctx->count(launch_ax_g32(sl, in, geom32.p, sync(), epi, a, ctx->stream));
+  else
+    ctx->count(launch_ax(sl, in, geom.p, sync(), epi, a, ctx->stream));
 }
 
-void semlab_space_s::apply_A(const double* in, double* out) {
+bool semlab_space_s::enable_geom32() {
+  if (order != 7) return false;
+  if (!has_geom32()) {
+    geom32.alloc(size_t(E) * 6 * size_t(nloc));
+    ctx->count(launch_to_f32(geom.p, geom32.p, E * 6 * nloc, ctx->stream));
+  }
+  return true;
+}
+
+void semlab_space_s::apply_A(const double* in, double* out, bool g32) {
   if (in == out) invalid("apply_A: in and out must not alias");
   EpiArgs a;
   a.w = out;
-  ax(in, Epi::Write, a);
+  ax(in, Epi::Write, a, g32);
   interface_sum(out);
   if (bc == SEMLAB_BC_NEUMANN) {  // r -= mean(r) (sem_space.cpp:207)
     static thread_local DevBuf<double> ones;
@@ -241,7 +253,7 @@ double semlab_space_s::dot(const double* a, const double* b) {
 // ------------------------------------------------------------------------------ operators
 void semlab_op_s::apply(const double* in, double* out) {
   switch (kind) {
-    case kA: space->apply_A(in, out); break;
+    case kA: space->apply_A(in, out, geom32); break;
     case kJacobi: ctx->count(launch_mul(out, space->jacobi_inv(), in, n, ctx->stream)); break;
     case kSchwarz: sch->apply(in, out); break;
     case kPmg: pmg->vcycle(in, out); break;

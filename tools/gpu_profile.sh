@@ -14,7 +14,7 @@ if [ "${FULL_ONLY:-0}" = "0" ]; then
 fi
 if [ "${NCU:-1}" = "1" ]; then
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-      -k regex:"${KREGEX:-k_axp|k_ras<\(int\)10|k_pass|k_cgs_update_dot|k_gemv_t}" -s ${SKIP:-60} -c ${COUNT:-16} \
+      -k regex:"${KREGEX:-k_axw|k_rasw|k_pass|k_cgs_update_dot|k_gemv_t}" -s ${SKIP:-60} -c ${COUNT:-16} \
       --nvtx --nvtx-include "timed/" -o gpurun_out/full_$R${TAG:-} -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_$R${TAG:-}.log 2>&1
 fi
 exit 0
