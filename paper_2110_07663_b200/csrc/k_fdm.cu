@@ -32,6 +32,10 @@ constexpr int kGatherUnroll = SEMLAB_RASW_GATHER_UNROLL;
 #define SEMLAB_RASW_MINB 5  // resident 4-warp CTAs per SM the warp-per-element RAS is register-capped for
 #endif
 
+#ifndef SEMLAB_RASW_FFMA2
+#define SEMLAB_RASW_FFMA2 1  // packed FP32 FMA (sm_100 FFMA2) in the FDM line passes
+#endif
+
 namespace sb {
 
 namespace {
@@ -402,7 +406,19 @@ __device__ __forceinline__ void wfwd(const T* __restrict__ src, const T* __restr
     T xa[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) xa[r] = src[base[r] + a * stride];
-    if constexpr (P % 2 == 0) {
+    if constexpr (P % 2 == 0 && sizeof(T) == 4 && SEMLAB_RASW_FFMA2) {
+      // packed FP32 (FFMA2): the (o, o+1) output pair shares x_a; same per-output order as below
+#pragma unroll
+      for (int o = 0; o < P; o += 2) {
+        const float2 s2 = *reinterpret_cast<const float2*>(M + a * P + o);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float2 acc = __ffma2_rn(s2, make_float2(xa[r], xa[r]), make_float2(y[r][o], y[r][o + 1]));
+          y[r][o] = acc.x;
+          y[r][o + 1] = acc.y;
+        }
+      }
+    } else if constexpr (P % 2 == 0) {
 #pragma unroll
       for (int o = 0; o < P; o += 2) {
         T s0, s1;
@@ -436,7 +452,20 @@ __device__ __forceinline__ void wbwd(const T (&x)[WShape<P, T>::R][P], const T* 
     T acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = T(0);
-    if constexpr (P % 2 == 0) {
+    if constexpr (P % 2 == 0 && sizeof(T) == 4 && SEMLAB_RASW_FFMA2) {
+      // packed FP32: even and odd o accumulate in the two halves, summed at the end
+      float2 a2[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a2[r] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int o = 0; o < P; o += 2) {
+        const float2 s2 = *reinterpret_cast<const float2*>(M + a * P + o);
+#pragma unroll
+        for (int r = 0; r < R; ++r) a2[r] = __ffma2_rn(s2, make_float2(x[r][o], x[r][o + 1]), a2[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = a2[r].x + a2[r].y;
+    } else if constexpr (P % 2 == 0) {
 #pragma unroll
       for (int o = 0; o < P; o += 2) {
         T s0, s1;
@@ -471,6 +500,10 @@ __device__ __forceinline__ void wbases(int lane, int (&base)[WShape<P, T>::R], b
   }
 }
 
+#ifndef SEMLAB_RASW_PF
+#define SEMLAB_RASW_PF 0  // L2 prefetch of the next element's box rows and factors
+#endif
+
 template <int P, class T, int MODE>
 __global__ void __launch_bounds__(WShape<P, T>::NT, sizeof(T) == 4 ? SEMLAB_RASW_MINB : 2)
     k_rasw(const Slab sl, const T* __restrict__ S, const T* __restrict__ L, const double* __restrict__ rin,
@@ -488,6 +521,24 @@ __global__ void __launch_bounds__(WShape<P, T>::NT, sizeof(T) == 4 ? SEMLAB_RASW
   for (int el = blockIdx.x * W::WPC + warp; el < nE; el += gridDim.x * W::WPC) {
     const int ex = el % sl.Ex, ey = (el / sl.Ex) % sl.Ey, ez = sl.ez0 + el / (sl.Ex * sl.Ey);
     const Box1D X = box1d(ex, sl.Ex, sl.q, dir), Y = box1d(ey, sl.Ey, sl.q, dir), Z = box1d(ez, sl.Ez, sl.q, dir);
+#if SEMLAB_RASW_PF
+    {  // the next element's extended-box rows (and factors) -> L2 while this element is solved
+      const int en = el + gridDim.x * W::WPC;
+      if (en < nE) {
+        const int nx = en % sl.Ex, ny = (en / sl.Ex) % sl.Ey, nz = sl.ez0 + en / (sl.Ex * sl.Ey);
+        const Box1D NX = box1d(nx, sl.Ex, sl.q, dir), NY = box1d(ny, sl.Ey, sl.q, dir), NZ = box1d(nz, sl.Ez, sl.q, dir);
+        const double* nc = rin + sl.lidx(NX.lo, NY.lo, NZ.lo);
+        const int64_t NXY = sl.Nx * sl.Ny;
+        for (int rw = lane; rw < NY.n * NZ.n; rw += 32) {
+          const double* p = nc + (rw % NY.n) * sl.Nx + (rw / NY.n) * NXY;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p + NX.n - 1));
+        }
+        if (lane < (3 * P2 * int(sizeof(T)) + 127) / 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(S + int64_t(en) * 3 * P2) + lane * 128));
+      }
+    }
+#endif
     __syncwarp();  // the previous element's owner write has finished reading tmp
     {  // factors: S (3 P^2) and lambda (3 P), all loads issued before the stores
       constexpr int NF = 3 * P2 + 3 * P, IT = (NF + 31) / 32;

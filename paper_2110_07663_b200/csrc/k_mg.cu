@@ -28,11 +28,15 @@ __device__ __forceinline__ bool on_boundary(int64_t x, int64_t y, int64_t z, con
 // RESTRICT: out[I] = sum over the 1-D support of coarse node I of J(i, a) in[X] (each X once)
 // The pass axis is a template parameter and the output coordinates come from 32-bit divisions
 // (the launcher checks the extents), so the index arithmetic stays off the critical path.
-template <bool PROLONG, int AXIS>
+// QF/QC > 0: the orders are compile-time constants (the (7,3,1) schedule), so the 1-D support
+// loops unroll and the element divisions become multiplications; 0: runtime orders.
+template <bool PROLONG, int AXIS, int QF, int QC>
 __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, const Grid3 gin, double* __restrict__ out,
-                                              const Grid3 gout, const Jmat J, const int qf, const int qc,
+                                              const Grid3 gout, const Jmat J, const int qf_rt, const int qc_rt,
                                               const int E_axis, const int mask_in, const Grid3 gmask_in,
-                                              const int mask_out, const Grid3 gmask_out, const int zb, const int nz) {
+                                              const int mask_out, const Grid3 gmask_out, const int zb, const int nz,
+                                              const int add_out) {
+  const int qf = QF > 0 ? QF : qf_rt, qc = QC > 0 ? QC : qc_rt;
   const unsigned nx = unsigned(gout.N[0]), ny = unsigned(gout.N[1]);
   const unsigned total = nx * ny * unsigned(nz);
   const int jn = qc + 1;  // J is (qf+1) x (qc+1), row-major
@@ -42,7 +46,7 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
     const unsigned row = t / nx;
     const int c[3] = {int(t - row * nx), int(row % ny), zb + int(row / ny)};
     if (mask_out && gmask_out.dirichlet && on_boundary(c[0], c[1], c[2], gmask_out)) {
-      out[gout.idx(c[0], c[1], c[2])] = 0.0;
+      if (!add_out) out[gout.idx(c[0], c[1], c[2])] = 0.0;  // (add: out += 0)
       continue;
     }
     // input row through this point along AXIS; the other two coordinates fix the mask test
@@ -69,7 +73,9 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
         e -= 1;
         i = qf;
       }
-      for (int a = 0; a < jn; ++a) {
+#pragma unroll
+      for (int a = 0; a < (QC > 0 ? QC + 1 : 16); ++a) {
+        if (QC == 0 && a >= jn) break;
         const double w = J.v[i * jn + a];
         if (w != 0.0) acc += w * fetch(e * qc + a);
       }
@@ -81,25 +87,32 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
         // (on a slab, an element of the other rank contributes through the interface sum; the
         // shared fine node X = e qf is counted with the left element only)
         if (e - 1 >= J.e_lo)
-          for (int i = 0; i <= qf; ++i) {
+#pragma unroll
+          for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
+            if (QF == 0 && i > qf) break;
             const double w = J.v[i * jn + qc];
             if (w != 0.0) acc += w * fetch((e - 1) * qf + i);
           }
         if (e < E_axis && e < J.e_hi)
-          for (int i = 1; i <= qf; ++i) {
+#pragma unroll
+          for (int i = 1; i < (QF > 0 ? QF + 1 : 16); ++i) {
+            if (QF == 0 && i > qf) break;
             const double w = J.v[i * jn + 0];
             if (w != 0.0) acc += w * fetch(e * qf + i);
           }
       } else {
         if (e == E_axis) e -= 1;  // last coarse node belongs to the last element
         const int aa = I - e * qc;
-        for (int i = 0; i <= qf; ++i) {
+#pragma unroll
+        for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
+          if (QF == 0 && i > qf) break;
           const double w = J.v[i * jn + aa];
           if (w != 0.0) acc += w * fetch(e * qf + i);
         }
       }
     }
-    out[gout.idx(c[0], c[1], c[2])] = acc;
+    double* o = out + gout.idx(c[0], c[1], c[2]);
+    *o = add_out ? *o + acc : acc;  // add: the coarse correction x += P e fused into the last pass
   }
 }
 
@@ -107,21 +120,28 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
 
 int64_t launch_transfer_pass(bool prolong, const double* in, const Grid3& gin, double* out, const Grid3& gout,
                              int axis, const Jmat& J, int qf, int qc, int E_axis, bool mask_in, const Grid3& gmi,
-                             bool mask_out, const Grid3& gmo, int64_t zb, int64_t nz, cudaStream_t s) {
+                             bool mask_out, const Grid3& gmo, int64_t zb, int64_t nz, cudaStream_t s, bool add_out) {
   const int64_t total = gout.N[0] * gout.N[1] * nz;
   if (total <= 0) return 0;
   if (total >= (int64_t(1) << 32) || gmi.N[2] >= (int64_t(1) << 31) || zb >= (int64_t(1) << 31))
     invalid("transfer pass: lattice too large for 32-bit pass indexing");
   if (axis < 0 || axis > 2) invalid("transfer pass: axis must be 0, 1 or 2");
-#define L_(PR, AX)                                                                                            \
-  k_pass<PR, AX><<<grid_for(total), 256, 0, s>>>(in, gin, out, gout, J, qf, qc, E_axis, mask_in, gmi, mask_out, \
-                                                  gmo, int(zb), int(nz))
+#define L3_(PR, AX, QF, QC)                                                                                       \
+  k_pass<PR, AX, QF, QC><<<grid_for(total), 256, 0, s>>>(in, gin, out, gout, J, qf, qc, E_axis, mask_in, gmi, mask_out, \
+                                                          gmo, int(zb), int(nz), int(add_out))
+#define L_(PR, AX)                                     \
+  do {                                                 \
+    if (qf == 7 && qc == 3) L3_(PR, AX, 7, 3);         \
+    else if (qf == 3 && qc == 1) L3_(PR, AX, 3, 1);    \
+    else L3_(PR, AX, 0, 0);                            \
+  } while (0)
   if (prolong) {
     if (axis == 0) L_(true, 0); else if (axis == 1) L_(true, 1); else L_(true, 2);
   } else {
     if (axis == 0) L_(false, 0); else if (axis == 1) L_(false, 1); else L_(false, 2);
   }
 #undef L_
+#undef L3_
   SB_LAUNCH_CHECK();
   return 1;
 }

@@ -529,7 +529,7 @@ void semlab_pmg_s::build() {
 }
 
 // P: coarse level l+1 -> fine level l (three 1-D passes: z, y, x)
-void semlab_pmg_s::prolong(int l, const double* cv, double* fv) {
+void semlab_pmg_s::prolong(int l, const double* cv, double* fv, bool add) {
   const Slab& f = lv[size_t(l)].sp->sl;
   const Slab& c = lv[size_t(l) + 1].sp->sl;
   const int qf = f.q, qc = c.q;
@@ -544,7 +544,7 @@ void semlab_pmg_s::prolong(int l, const double* cv, double* fv) {
   const int64_t zb = int64_t(f.ez0) * qf, nz = int64_t(f.ez1 - f.ez0) * qf + 1;
   ctx->count(launch_transfer_pass(true, cv, gc, tA.p, g1, 2, J[size_t(l)], qf, qc, f.Ez, true, gc, false, gf, zb, nz, s));
   ctx->count(launch_transfer_pass(true, tA.p, g1, tB.p, g2, 1, J[size_t(l)], qf, qc, f.Ey, false, gc, false, gf, zb, nz, s));
-  ctx->count(launch_transfer_pass(true, tB.p, g2, fv, gf, 0, J[size_t(l)], qf, qc, f.Ex, false, gc, true, gf, zb, nz, s));
+  ctx->count(launch_transfer_pass(true, tB.p, g2, fv, gf, 0, J[size_t(l)], qf, qc, f.Ex, false, gc, true, gf, zb, nz, s, add));
 }
 
 // P^T: fine level l -> coarse level l+1 (passes x, y, z)
@@ -596,8 +596,7 @@ void semlab_pmg_s::cycle(int l) {
   }
   restrict_(l, L.r.p, lv[size_t(l) + 1].b.p);
   cycle(l + 1);
-  prolong(l, lv[size_t(l) + 1].x.p, L.r.p);
-  ctx->count(launch_axpby(L.x.p, 1.0, L.r.p, 1.0, n, s));
+  prolong(l, lv[size_t(l) + 1].x.p, L.x.p, true);  // x += P e_C (fused into the last pass)
   L.cheb->smooth(L.b.p, L.x.p, false);
 }
 

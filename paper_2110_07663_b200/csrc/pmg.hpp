@@ -85,7 +85,7 @@ struct semlab_pmg_s {
   semlab_space coarse_full = nullptr;  // whole-mesh p=1 space for the redundant coarse solve
   ~semlab_pmg_s();
   void build();
-  void prolong(int l, const double* coarse_v, double* fine_v);
+  void prolong(int l, const double* coarse_v, double* fine_v, bool add = false);  // add: fine_v += P coarse_v
   void restrict_(int l, const double* fine_v, double* coarse_v);
   void vcycle(const double* b, double* z);
   void cycle(int l);
