@@ -32,6 +32,9 @@ constexpr int kGatherUnroll = SEMLAB_RASW_GATHER_UNROLL;
 #define SEMLAB_RASW_MINB 5  // resident 4-warp CTAs per SM the warp-per-element RAS is register-capped for
 #endif
 
+#ifndef SEMLAB_RASW_MINP
+#define SEMLAB_RASW_MINP 8  // warp-per-element RAS from box size P = p + 3 >= this (p >= 3)
+#endif
 #ifndef SEMLAB_RASW_FFMA2
 #define SEMLAB_RASW_FFMA2 1  // packed FP32 FMA (sm_100 FFMA2) in the FDM line passes
 #endif
@@ -345,10 +348,16 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_ras(const Slab 
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (ok[u]) {
-          epi.x[g[u]] = xv[u] + dv[u];
+          const double x1 = xv[u] + dv[u];
           const double rg = rv[u] - z[u];
-          epi.r[g[u]] = rg;
-          epi.d[g[u]] = epi.c1 * dv[u] + epi.c2 * rg;
+          const double dn = epi.c1 * dv[u] + epi.c2 * rg;
+          if (MODE == 3) {  // last step: the final x += d fused, r and d are dead afterwards
+            epi.x[g[u]] = x1 + dn;
+          } else {
+            epi.x[g[u]] = x1;
+            epi.r[g[u]] = rg;
+            epi.d[g[u]] = dn;
+          }
         }
     }
   }
@@ -678,10 +687,16 @@ __global__ void __launch_bounds__(WShape<P, T>::NT, sizeof(T) == 4 ? SEMLAB_RASW
 #pragma unroll
           for (int u = 0; u < U; ++u)
             if (ok[u]) {
-              epi.x[g[u]] = xv[u] + dv[u];
+              const double x1 = xv[u] + dv[u];
               const double rg = rv[u] - z[u];
-              epi.r[g[u]] = rg;
-              epi.d[g[u]] = epi.c1 * dv[u] + epi.c2 * rg;
+              const double dn = epi.c1 * dv[u] + epi.c2 * rg;
+              if (MODE == 3) {  // last step: the final x += d fused, r and d are dead afterwards
+                epi.x[g[u]] = x1 + dn;
+              } else {
+                epi.x[g[u]] = x1;
+                epi.r[g[u]] = rg;
+                epi.d[g[u]] = dn;
+              }
             }
         }
       }
@@ -804,10 +819,11 @@ struct Launch {
   }
   template <int P>
   static void ras(const Slab& sl, const T* S, const T* L, const double* r, int mode, const RasEpi& e, cudaStream_t s) {
-    if (sizeof(T) == 4 && P >= 8 && ras_warp() && sl.elems() < (int64_t(1) << 31)) {
+    if (sizeof(T) == 4 && P >= SEMLAB_RASW_MINP && ras_warp() && sl.elems() < (int64_t(1) << 31)) {
       if (mode == 0) rasw<P, 0>(sl, S, L, r, e, s);
       else if (mode == 1) rasw<P, 1>(sl, S, L, r, e, s);
-      else rasw<P, 2>(sl, S, L, r, e, s);
+      else if (mode == 2) rasw<P, 2>(sl, S, L, r, e, s);
+      else rasw<P, 3>(sl, S, L, r, e, s);
       return;
     }
     using Sh = Shape<P, T>;
@@ -818,9 +834,12 @@ struct Launch {
     } else if (mode == 1) {
       prep(k_ras<P, T, 1>, Sh::smem());
       k_ras<P, T, 1><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, r, e);
-    } else {
+    } else if (mode == 2) {
       prep(k_ras<P, T, 2>, Sh::smem());
       k_ras<P, T, 2><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, r, e);
+    } else {
+      prep(k_ras<P, T, 3>, Sh::smem());
+      k_ras<P, T, 3><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, r, e);
     }
   }
   template <int P>

@@ -26,6 +26,9 @@
 #ifndef SEMLAB_AX_BATCH_EPI
 #define SEMLAB_AX_BATCH_EPI 1  // owner epilogue: issue all vector loads before the stores
 #endif
+#ifndef SEMLAB_AX_SPLIT_ND
+#define SEMLAB_AX_SPLIT_ND 6  // orders p <= 5: element-local Ax + ordered gather (no counter waits)
+#endif
 #ifndef SEMLAB_AXP_MINB
 #define SEMLAB_AXP_MINB 6  // resident CTAs per SM the persistent Ax is register-capped for
 #endif
@@ -186,7 +189,9 @@ constexpr int ax_min_blocks() {  // occupancy target: caps registers so ~20 warp
   return ND >= 8 ? 10 : 16;
 }
 
-template <int ND, int EPB, bool LOCAL, class EpiT>
+// IO: 0 global -> global with the owner-ordered Q^T; 1 local -> local (E-vectors); 2 global in,
+// element-local out (the split path: k_gather_epi then sums in the reference order)
+template <int ND, int EPB, int IO, class EpiT>
 __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
     k_ax(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const double* __restrict__ geom,
          double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int ngroups,
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
 
   if (tid == 0) {
     int t;
-    if (LOCAL) {
+    if (IO != 0) {
       t = blockIdx.x;
     } else {
       t = int(atomicAdd(ticket, 1u));
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
     const int lines = (ne * 6 * NLOC * int(sizeof(double)) + 127) / 128;
     for (int l = tid; l < lines; l += NT) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + size_t(l) * 128));
   }
-  if (tid == 0 && !LOCAL) s_epoch = *reinterpret_cast<volatile unsigned*>(&flags[e0]);
+  if (tid == 0 && IO == 0) s_epoch = *reinterpret_cast<volatile unsigned*>(&flags[e0]);
 
   const int le = tid / ND2, ij = tid % ND2, i = ij % ND, j = ij / ND;
   const bool active = le < ne;
@@ -238,8 +243,8 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
   double ureg[ND];
 #pragma unroll
   for (int k = 0; k < ND; ++k) {  // unconditional loads (el is clamped to a valid element), then select
-    const double raw = LOCAL ? __ldg(&u[el * NLOC + k * ND2 + ij]) : __ldg(&u[sl.lidx(x, y, zb + k)]);
-    const double v = (!active || (!LOCAL && sl.masked(x, y, zb + k))) ? 0.0 : raw;
+    const double raw = IO == 1 ? __ldg(&u[el * NLOC + k * ND2 + ij]) : __ldg(&u[sl.lidx(x, y, zb + k)]);
+    const double v = (!active || (IO != 1 && sl.masked(x, y, zb + k))) ? 0.0 : raw;
     ureg[k] = v;
     sa[k * ND2 + ij] = v;
   }
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
     out[k] = acc;
   }
 
-  if (LOCAL) {
+  if (IO != 0) {
     if (active)
 #pragma unroll
       for (int k = 0; k < ND; ++k) out_local[el * NLOC + k * ND2 + ij] = out[k];
@@ -712,6 +717,9 @@ int64_t axp_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
 // i = 2(lane%4) + {0,1}), the D-fragments live in 4 registers, and the per-warp shared
 // workspace (3 arrays of 8 z-layers) is padded and XOR-swizzled so every fragment access is
 // conflict-free (2 wavefronts per 256 B).
+#ifndef SEMLAB_AXW_EXP
+#define SEMLAB_AXW_EXP 0  // timing experiments (wrong results): 1 no Q^T finish, 2 no DMMA
+#endif
 namespace axw {
 constexpr int PS = 72;  // z-layer stride (doubles): 64 + 8 so consecutive layers use opposite bank halves
 constexpr int ARR = 8 * PS;
@@ -719,6 +727,11 @@ __device__ __forceinline__ int sidx(int k, int j, int i) {  // swizzled workspac
   return k * PS + j * 8 + 2 * ((i >> 1) ^ ((j >> 1) & 3)) + (i & 1);
 }
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  if (SEMLAB_AXW_EXP == 2) {  // timing experiment only: no tensor-core work
+    c0 += a;
+    c1 += b;
+    return;
+  }
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
@@ -1040,7 +1053,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
     }
     // the release of this element is deferred until the next element's u has been gathered
     // (its MEMBAR then finds the deposits long acknowledged instead of stalling the warp)
-    if (prev >= 0) finish_prev(prev);
+    if (prev >= 0 && SEMLAB_AXW_EXP != 1) finish_prev(prev);
 #if !SEMLAB_AXW_PDEP
 #pragma unroll
     for (int t = 0; t < 16; ++t) pprev[t] = o[t];
@@ -1052,7 +1065,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
   }
   __syncwarp();
   if (lane == 0) st_release(&flags[prev], target);
-  finish_prev(prev);
+  if (SEMLAB_AXW_EXP != 1) finish_prev(prev);
 }
 
 template <class EpiT, class GT>
@@ -1090,6 +1103,56 @@ bool ax_dmma() {  // SEMLAB_AX_DMMA=0 selects the FP64-FMA persistent kernel (A/
   return on;
 }
 
+struct Cands {  // elements (along one axis) containing a lattice coordinate, ascending
+  int n;
+  int e[2];
+  int loc[2];
+};
+__device__ __forceinline__ Cands cands(int64_t c, int q, int Eax, int lo_elem, int hi_elem) {
+  // hi_elem = one past the last element layer available locally
+  Cands r;
+  int64_t e = c / q;
+  const int l = int(c % q);
+  if (l == 0 && e > 0) {
+    r.n = 0;
+    if (e - 1 >= lo_elem) { r.e[r.n] = int(e - 1); r.loc[r.n] = q; ++r.n; }
+    if (e < hi_elem) { r.e[r.n] = int(e); r.loc[r.n] = 0; ++r.n; }
+  } else {
+    if (e == Eax) { e -= 1; }
+    r.n = 1;
+    r.e[0] = int(e);
+    r.loc[0] = (e * q == c) ? 0 : int(c - e * q);
+  }
+  return r;
+}
+
+// Q^T of element-local results with an owner epilogue: each lattice node sums its <= 8
+// contributors in ascending element id (sem_space.cpp:110-119 order), masked nodes get 0.
+template <int ND, class EpiT>
+__global__ void __launch_bounds__(256) k_gather_epi(const Slab sl, const double* __restrict__ loc, const EpiT epi) {
+  constexpr int q = ND - 1, NLOC = ND * ND * ND;
+  const int64_t zb = int64_t(sl.ez0) * q, nz = int64_t(sl.ez1 - sl.ez0) * q + 1;
+  const int64_t total = sl.Nx * sl.Ny * nz;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t x = t % sl.Nx, y = (t / sl.Nx) % sl.Ny, z = zb + t / (sl.Nx * sl.Ny);
+    const int64_t g = sl.lidx(x, y, z);
+    if (sl.masked(x, y, z)) {
+      epi(g, 0.0);
+      continue;
+    }
+    const Cands cx = cands(x, q, sl.Ex, 0, sl.Ex), cy = cands(y, q, sl.Ey, 0, sl.Ey);
+    const Cands cz = cands(z, q, sl.Ez, sl.ez0, sl.ez1);
+    double acc = 0.0;
+    for (int c = 0; c < cz.n; ++c)
+      for (int b = 0; b < cy.n; ++b)
+        for (int a = 0; a < cx.n; ++a) {
+          const int64_t el = cx.e[a] + int64_t(sl.Ex) * (cy.e[b] + int64_t(sl.Ey) * (cz.e[c] - sl.ez0));
+          acc += loc[el * NLOC + cx.loc[a] + ND * (cy.loc[b] + ND * cz.loc[c])];
+        }
+    epi(g, acc);
+  }
+}
+
 template <int ND, bool LOCAL, class EpiT>
 int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, const AxSync& sy, double* out_local,
                        const EpiT& epi, cudaStream_t s) {
@@ -1105,15 +1168,24 @@ int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, cons
   if (nE == 0) return 0;
   const int ngroups = int((nE + EPB - 1) / EPB);
   const size_t smem = (size_t(EPB) * 2 * NLOC + ND * ND) * sizeof(double);
-  auto kern = k_ax<ND, EPB, LOCAL, EpiT>;
+  // low orders: element-local Ax into the deposit buffer, then the ordered gather with the
+  // epilogue (two fully parallel launches instead of CTAs idling on neighbour counters)
+  constexpr int IO = LOCAL ? 1 : (ND <= SEMLAB_AX_SPLIT_ND ? 2 : 0);
+  auto kern = k_ax<ND, EPB, IO, EpiT>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = true;
   }
   kern<<<ngroups, EPB * ND * ND, smem, s>>>(sl, dmat<ND>(sl.q), u, geom, sy.dep, sy.flags, sy.ticket, ngroups,
-                                           out_local, epi);
+                                           IO == 2 ? sy.dep : out_local, epi);
   SB_LAUNCH_CHECK();
+  if constexpr (IO == 2) {
+    const int64_t total = sl.Nx * sl.Ny * (int64_t(sl.ez1 - sl.ez0) * sl.q + 1);
+    k_gather_epi<ND><<<grid1d(total, 256), 256, 0, s>>>(sl, sy.dep, epi);
+    SB_LAUNCH_CHECK();
+    return 2;
+  }
   return 1;
 }
 
@@ -1159,28 +1231,6 @@ __global__ void k_local_diag(const Slab sl, const DMat<ND> Dm, const double* __r
 }
 
 // ------------------------------------------------------------------------ Q, Q^T, QQ^T
-struct Cands {  // elements (along one axis) containing a lattice coordinate, ascending
-  int n;
-  int e[2];
-  int loc[2];
-};
-__device__ __forceinline__ Cands cands(int64_t c, int q, int Eax, int lo_elem, int hi_elem) {
-  // hi_elem = one past the last element layer available locally
-  Cands r;
-  int64_t e = c / q;
-  const int l = int(c % q);
-  if (l == 0 && e > 0) {
-    r.n = 0;
-    if (e - 1 >= lo_elem) { r.e[r.n] = int(e - 1); r.loc[r.n] = q; ++r.n; }
-    if (e < hi_elem) { r.e[r.n] = int(e); r.loc[r.n] = 0; ++r.n; }
-  } else {
-    if (e == Eax) { e -= 1; }
-    r.n = 1;
-    r.e[0] = int(e);
-    r.loc[0] = (e * q == c) ? 0 : int(c - e * q);
-  }
-  return r;
-}
 
 __global__ void k_gather(const Slab sl, const double* __restrict__ loc, double* __restrict__ out) {
   const int q = sl.q, nd = q + 1;

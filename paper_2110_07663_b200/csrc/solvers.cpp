@@ -121,10 +121,10 @@ void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
       es.d = d.p;
       es.c1 = rho_next * rho;
       es.c2 = 2.0 * rho_next / delta;
-      sch->ras(t.p, 2, es);
+      sch->ras(t.p, k == params.order ? 3 : 2, es);  // 3: the final x += d fused
       rho = rho_next;
     }
-    ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));
+    if (params.order == 0) ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));
     return;
   }
   // generic surrogate S
