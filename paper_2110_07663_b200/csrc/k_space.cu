@@ -717,6 +717,9 @@ int64_t axp_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
 // i = 2(lane%4) + {0,1}), the D-fragments live in 4 registers, and the per-warp shared
 // workspace (3 arrays of 8 z-layers) is padded and XOR-swizzled so every fragment access is
 // conflict-free (2 wavefronts per 256 B).
+#ifndef SEMLAB_AXW_TMA
+#define SEMLAB_AXW_TMA 0  // whole-element geometry by one TMA bulk copy into shared memory, one element ahead
+#endif
 #ifndef SEMLAB_AXW_EXP
 #define SEMLAB_AXW_EXP 0  // timing experiments (wrong results): 1 no Q^T finish, 2 no DMMA
 #endif
@@ -739,7 +742,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }  // namespace axw
 
 #ifndef SEMLAB_AXW_WARPS
-#define SEMLAB_AXW_WARPS 4  // warps (independent element pipelines) per CTA
+#define SEMLAB_AXW_WARPS (SEMLAB_AXW_TMA ? 1 : 4)  // warps (independent element pipelines) per CTA
 #endif
 #ifndef SEMLAB_AXW_GPF
 #define SEMLAB_AXW_GPF 2  // geometry L2 prefetch: 0 none, 1 one element ahead, 2 current element, 3 bulk (current)
@@ -748,12 +751,23 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #define SEMLAB_AXW_PDEP 1  // face-owned results wait in the element's deposit slots, not registers
 #endif
 #ifndef SEMLAB_AXW_MINB
-#define SEMLAB_AXW_MINB 3  // resident CTAs per SM (register cap 168)
+#define SEMLAB_AXW_MINB (SEMLAB_AXW_TMA ? 5 : 3)  // resident CTAs per SM
 #endif
+
+template <class GT>
+__host__ __device__ constexpr int axw_warp_doubles() {  // per-warp shared memory in doubles
+  return 3 * axw::ARR + (SEMLAB_AXW_TMA ? 6 * 512 * int(sizeof(GT)) / 8 : 0);
+}
 
 __device__ __forceinline__ double2 ld_geom2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ double2 ld_geom2(const float* p) {
   const float2 v = __ldcs(reinterpret_cast<const float2*>(p));
+  return make_double2(double(v.x), double(v.y));
+}
+
+__device__ __forceinline__ double2 ld_geom2_smem(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ double2 ld_geom2_smem(const float* p) {
+  const float2 v = *reinterpret_cast<const float2*>(p);
   return make_double2(double(v.x), double(v.y));
 }
 
@@ -768,9 +782,13 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
   constexpr int ND = 8, ND2 = 64, NLOC = 512, q = 7;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* sU = reinterpret_cast<double*>(smem_raw) + size_t(wid) * 3 * ARR;  // u, then Gr
-  double* sS = sU + ARR;                                                      // Gs
-  double* sT = sS + ARR;                                                      // ut, Gt, then D^T Gt
+  double* sU = reinterpret_cast<double*>(smem_raw) + size_t(wid) * axw_warp_doubles<GT>();  // u, then Gr
+  double* sS = sU + ARR;                                                                 // Gs
+  double* sT = sS + ARR;                                                                 // ut, Gt, then D^T Gt
+  GT* sGeo = reinterpret_cast<GT*>(sT + ARR);  // SEMLAB_AXW_TMA: the element's 6 factor planes
+  uint64_t* gbar = reinterpret_cast<uint64_t*>(smem_raw + size_t(SEMLAB_AXW_WARPS) * axw_warp_doubles<GT>() * 8) + wid;
+  constexpr unsigned GBYTES = 6 * 512 * sizeof(GT);
+  unsigned gphase = 0;
   const int gj = lane >> 2, gc = lane & 3;  // fragment row / column group
   const int j = gj, i0 = 2 * gc;            // this lane's nodes: (k, j, i0 + {0,1})
   // D fragments: Df[kc] = D(lane/4, lane%4 + 4kc), Dt[kc] = D(lane%4 + 4kc, lane/4)
@@ -820,6 +838,11 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
   int el = take();
   if (el >= nE) return;
   const unsigned target = *reinterpret_cast<volatile unsigned*>(&flags[el]) + 1u;
+  if (SEMLAB_AXW_TMA && lane == 0) {  // this element's geometry -> shared memory (TMA engine)
+    mbar_init(gbar, 1);
+    mbar_expect_tx(gbar, GBYTES);
+    bulk_g2s(sGeo, geom + size_t(el) * 6 * NLOC, GBYTES, gbar);
+  }
   int prev = -1;
 #if !SEMLAB_AXW_PDEP
   double pprev[16];  // face-owned results of ticket t-1 ([k][i - i0])
@@ -916,7 +939,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
 
   int nxt = take();
   while (true) {
-    if (SEMLAB_AXW_GPF >= 2) prefetch_geom(el);
+    if (!SEMLAB_AXW_TMA && SEMLAB_AXW_GPF >= 2) prefetch_geom(el);
     prefetch(nxt);
     const int ex = el % Ex, ey = (el / Ex) % Ey, ez = sl.ez0 + el / LZ;
     const int y = ey * q + j, zb = ez * q;
@@ -955,13 +978,21 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
     // per z-layer: ur, us (DMMA), ut (workspace), geometric factors, then Gr/Gs/Gt back out
     const GT* ge = geom + size_t(el) * 6 * NLOC + j * ND + i0;
     double2 gA[6], gB[6];
+    if (SEMLAB_AXW_TMA) {
+      mbar_wait(gbar, gphase);
+      gphase ^= 1u;
+    } else {
 #pragma unroll
-    for (int c = 0; c < 6; ++c) gA[c] = ld_geom2(ge + c * NLOC);
+      for (int c = 0; c < 6; ++c) gA[c] = ld_geom2(ge + c * NLOC);
+    }
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       double2* gcur = (k & 1) ? gB : gA;
       double2* gnext = (k & 1) ? gA : gB;
-      if (k + 1 < ND) {
+      if (SEMLAB_AXW_TMA) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) gcur[c] = ld_geom2_smem(sGeo + c * NLOC + k * ND2 + j * ND + i0);
+      } else if (k + 1 < ND) {
 #pragma unroll
         for (int c = 0; c < 6; ++c)
           gnext[c] = ld_geom2(ge + c * NLOC + (k + 1) * ND2);
@@ -992,6 +1023,11 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
       *reinterpret_cast<double2*>(sT + sidx(k, j, i0)) = make_double2(gt[0], gt[1]);
     }
     __syncwarp();
+    if (SEMLAB_AXW_TMA && lane == 0 && nxt < nE) {  // the next element's geometry streams in now
+      fence_proxy_async_shared();
+      mbar_expect_tx(gbar, GBYTES);
+      bulk_g2s(sGeo, geom + size_t(nxt) * 6 * NLOC, GBYTES, gbar);
+    }
     // out_k = Gr_k D + D^T Gs_k
     double o[16];
 #pragma unroll
@@ -1077,7 +1113,7 @@ int64_t axw_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
   if (sl.n_local() >= (int64_t(1) << 31) || nE * NLOC >= (int64_t(1) << 31))
     invalid("SemSpace: a rank's lattice must have < 2^31 nodes");
   constexpr int W = SEMLAB_AXW_WARPS;
-  const size_t smem = size_t(W) * 3 * axw::ARR * sizeof(double);
+  const size_t smem = size_t(W) * axw_warp_doubles<GT>() * sizeof(double) + size_t(W) * 8;
   auto kern = k_axw<EpiT, GT>;
   static int nctas = 0;
   if (nctas == 0) {
