@@ -64,9 +64,11 @@ __global__ void __launch_bounds__(kNT) k_gemv_t(const double* __restrict__ V, in
   for (int64_t t = int64_t(blockIdx.x) * kNT + threadIdx.x; t < len; t += int64_t(gridDim.x) * kNT) {
     const int64_t i = off + t;
     const double wi = w[i];
+    double v[NC];  // every column load issued before the first use (no per-column branch)
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < ncol) acc[c] = fma(__ldcs(V + c * ldv + i), wi, acc[c]);
+    for (int c = 0; c < NC; ++c) v[c] = c < ncol ? __ldcs(V + c * ldv + i) : 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = fma(v[c], wi, acc[c]);
   }
   finish_partials<NC>(acc, ncol, partial, counter, h);
 }
@@ -126,10 +128,13 @@ template <int NC>
 __global__ void __launch_bounds__(kNT) k_gemv_n(const double* __restrict__ V, int64_t ldv, int ncol, const Coef cf,
                                                 double* __restrict__ y, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * kNT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kNT) {
+    double v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = c < ncol ? V[c * ldv + i] : 0.0;
     double s = 0.0;
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      if (c < ncol) s += V[c * ldv + i] * cf.c[c];
+      if (c < ncol) s += v[c] * cf.c[c];
     y[i] = s;
   }
 }
