@@ -274,7 +274,7 @@ def run_ours(args, cfg, name):
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_summary.json")))
-        if prof.get("workload") == name:
+        if prof.get("workload") == name and world == 1:  # captured on one GPU (whole mesh per launch)
             traffic = prof.get("ax_dram_bytes_per_launch")
     except Exception:
         pass
