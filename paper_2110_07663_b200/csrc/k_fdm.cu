@@ -32,6 +32,9 @@ constexpr int kGatherUnroll = SEMLAB_RASW_GATHER_UNROLL;
 #define SEMLAB_RASW_MINB 5  // resident 4-warp CTAs per SM the warp-per-element RAS is register-capped for
 #endif
 
+#ifndef SEMLAB_RAS_SMALLP_MINB
+#define SEMLAB_RAS_SMALLP_MINB 5  // p = 3 level (P = 6): 5 CTAs/SM of the CTA RAS kernel
+#endif
 #ifndef SEMLAB_RASW_MINP
 #define SEMLAB_RASW_MINP 8  // warp-per-element RAS from box size P = p + 3 >= this (p >= 3)
 #endif
@@ -290,8 +293,13 @@ __device__ __forceinline__ void fdm_block(const Slab& sl, const T* __restrict__ 
 }
 
 // ---------------------------------------------------------------- RAS (+ fused Chebyshev update)
+template <int P, class T>
+constexpr int ras_minb() {  // CTAs per SM the CTA kernel is register-capped for
+  return sizeof(T) == 4 ? (P <= 7 ? SEMLAB_RAS_SMALLP_MINB : 3) : 1;
+}
+
 template <int P, class T, int MODE>
-__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_ras(const Slab sl, const T* __restrict__ S, const T* __restrict__ L,
+__global__ void __launch_bounds__(128, ras_minb<P, T>()) k_ras(const Slab sl, const T* __restrict__ S, const T* __restrict__ L,
                                              const double* __restrict__ r, RasEpi epi) {
   using Sh = Shape<P, T>;
   constexpr int P2 = Sh::P2, P3 = Sh::P3, EPC = Sh::EPC, SPE = Sh::SPE;

@@ -116,11 +116,11 @@ def main():
     open(os.path.join(PROF, f"{R}_launch_share.txt"), "w").write(launch_share(R))
     txt, js = full_summary(R)
     open(os.path.join(PROF, f"{R}_ncu_full.txt"), "w").write(txt)
-    ax = [v for k, v in js.items() if "k_axw" in k and "EWrite" in k]
+    ax = [v for k, v in js.items() if "k_axw" in k and "EWrite" in k and "double" in k]
     latest = {"round": R, "workload": workload, "kernels": js}
     if ax:
         latest["ax_dram_bytes_per_launch"] = ax[0]["dram__bytes_read.sum"] + ax[0]["dram__bytes_write.sum"]
-    ras = [v for k, v in js.items() if "k_rasw" in k]
+    ras = [v for k, v in js.items() if "k_rasw<10, float, 0>" in k]
     if ras:
         latest["ras_dram_bytes_per_launch"] = ras[0]["dram__bytes_read.sum"] + ras[0]["dram__bytes_write.sum"]
     json.dump(latest, open(os.path.join(PROF, "latest_ncu_summary.json"), "w"), indent=1)
