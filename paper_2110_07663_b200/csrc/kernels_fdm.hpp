@@ -8,7 +8,7 @@
 namespace sb {
 
 // Owner-write epilogue of the RAS kernel. mode 0: out = z. mode 1 (Chebyshev init):
-// r = z, d = z / c1. mode 2 (Chebyshev step): x += d; r -= z; d = c1 d + c2 r.
+// r = z, d = z * c2 (c2 = 1 / theta). mode 2 (Chebyshev step): x += d; r -= z; d = c1 d + c2 r.
 // mode 3 (last step): mode 2 followed by the final x += d, bit for bit; r and d not written.
 struct RasEpi {
   double* out = nullptr;

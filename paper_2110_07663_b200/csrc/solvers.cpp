@@ -100,6 +100,7 @@ void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
     e.r = r.p;
     e.d = d.p;
     e.c1 = theta;
+    e.c2 = 1.0 / theta;  // the init writes d = r * (1 / theta)
     if (x_is_zero) {
       sch->ras(b, 1, e);  // r = S (b - A 0) = S b
     } else {
