@@ -62,6 +62,8 @@ struct semlab_space_s {
   bool distributed() const { return !full && ctx->nranks > 1; }
   void halo_exchange(double* v);
   void owner_copy_up(double* v);
+  void interface_sum_halo(double* v);              // interface_sum + halo_exchange, one NCCL group
+  void owner_copy_up_n(double* const* vs, int k);  // owner_copy_up of k vectors, one NCCL group
 
   void build();
   sb::AxSync sync() const { return {dep.p, flags.p, ticket.p}; }

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "host_math.hpp"
 #include "schwarz.hpp"
@@ -18,6 +19,15 @@ cudaStream_t st(semlab_ctx c) { return c->stream; }
 
 // Fused Chebyshev-Jacobi needs S = diag(A)^-1 of the same space and a single rank (interface
 // planes need the cross-rank sum before the owner epilogue).
+// SEMLAB_DIST_FUSED=0 keeps the generic Chebyshev path on z-slabs (A/B).
+bool dist_ras_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SEMLAB_DIST_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool fused_jacobi(semlab_op S, semlab_op A) {
   return S->kind == semlab_op_s::kJacobi && A->kind == semlab_op_s::kA && S->space == A->space &&
          !A->space->distributed();
@@ -26,6 +36,12 @@ bool fused_jacobi(semlab_op S, semlab_op A) {
 bool fused_ras(semlab_op S, semlab_op A) {
   return S->kind == semlab_op_s::kSchwarz && S->sch->mode == SEMLAB_SCHWARZ_RAS && A->kind == semlab_op_s::kA &&
          S->space == A->space && !A->space->distributed();
+}
+
+bool dist_ras(semlab_op S, semlab_op A) {
+  return S->kind == semlab_op_s::kSchwarz && S->sch->mode == SEMLAB_SCHWARZ_RAS && A->kind == semlab_op_s::kA &&
+         S->space == A->space && A->space->distributed() && A->space->bc == SEMLAB_BC_DIRICHLET &&
+         dist_ras_enabled();
 }
 
 }  // namespace
@@ -123,6 +139,43 @@ void semlab_cheby_s::smooth(const double* b, double* x, bool x_is_zero) {
       es.c1 = rho_next * rho;
       es.c2 = 2.0 * rho_next / delta;
       sch->ras(t.p, k == params.order ? 3 : 2, es);  // 3: the final x += d fused
+      rho = rho_next;
+    }
+    if (params.order == 0) ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));
+    return;
+  }
+  if (dist_ras(S, A)) {
+    // RAS on z-slabs: the init stays generic; each Chebyshev step is t = A d (no interface sum
+    // yet), ONE grouped exchange (interface partials + Schwarz ghost planes), the RAS owner write
+    // carrying the Chebyshev update (mode 2, or 3 with the final x += d), and ONE grouped copy-up
+    // of the lower rank's interface plane. Owned nodes get exactly the generic path's values.
+    semlab_space sp = A->space;
+    semlab_schwarz_s* sch = S->sch;
+    if (x_is_zero) {
+      ctx->count(launch_copy(t.p, b, n, s));
+    } else {
+      A->apply(x, t.p);
+      ctx->count(launch_sub(t.p, b, t.p, n, s));
+    }
+    S->apply(t.p, r.p);
+    ctx->count(launch_cheb_init(r.p, d.p, theta, n, s));
+    double rho = 1.0 / sigma;
+    for (int k = 1; k <= params.order; ++k) {
+      const double rho_next = 1.0 / (2.0 * sigma - rho);
+      EpiArgs a;
+      a.w = t.p;
+      sp->ax(d.p, Epi::Write, a, A->geom32);
+      sp->interface_sum_halo(t.p);
+      RasEpi es;
+      es.x = x;
+      es.r = r.p;
+      es.d = d.p;
+      es.c1 = rho_next * rho;
+      es.c2 = 2.0 * rho_next / delta;
+      const bool last = k == params.order;
+      sch->ras(t.p, last ? 3 : 2, es);
+      double* vs[3] = {x, r.p, d.p};
+      sp->owner_copy_up_n(vs, last ? 1 : 3);
       rho = rho_next;
     }
     if (params.order == 0) ctx->count(launch_axpby(x, 1.0, d.p, 1.0, n, s));

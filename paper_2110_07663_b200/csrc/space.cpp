@@ -1,4 +1,5 @@
 // Context, mesh and SemSpace host logic (setup on the host/device, every apply on the device).
+#include <cstdlib>
 #include <nccl.h>
 #include <omp.h>
 
@@ -124,8 +125,17 @@ void semlab_space_s::build() {
 // Interface planes z = ez0 q (shared with rank-1) and z = ez1 q (shared with rank+1) hold this
 // rank's partial Q^T sums after a gather-type operation; both ranks add lower + upper partial in
 // that order, so the duplicated planes stay bitwise identical on the two ranks.
+// SEMLAB_NO_EXCHANGE=1 turns the slab exchanges into no-ops: timing experiments only (wrong results).
+static bool no_exchange() {
+  static const bool on = [] {
+    const char* e = std::getenv("SEMLAB_NO_EXCHANGE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 void semlab_space_s::interface_sum(double* v) {
-  if (!distributed()) return;
+  if (!distributed() || no_exchange()) return;
   const int64_t P = sl.Nx * sl.Ny;
   if (plane_lo.n < size_t(P)) {
     plane_lo.alloc(size_t(P));
@@ -150,9 +160,61 @@ void semlab_space_s::interface_sum(double* v) {
   if (sl.nranks_above) ctx->count(launch_add_planes(vt, vt, plane_hi.p, P, s));
 }
 
+// interface_sum followed by halo_exchange in ONE grouped NCCL call: right after a Q^T-type
+// operator the planes next to the interface are already final on their owner, so the partial
+// interface planes and the Schwarz ghost planes travel together (one latency instead of two).
+void semlab_space_s::interface_sum_halo(double* v) {
+  if (!distributed() || no_exchange()) return;
+  const int64_t P = sl.Nx * sl.Ny;
+  if (plane_lo.n < size_t(P)) {
+    plane_lo.alloc(size_t(P));
+    plane_hi.alloc(size_t(P));
+  }
+  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+  cudaStream_t s = ctx->stream;
+  const int r = ctx->rank;
+  const int64_t zb = int64_t(sl.ez0) * sl.q, zt = int64_t(sl.ez1) * sl.q;
+  double* vb = v + sl.lidx(0, 0, zb);
+  double* vt = v + sl.lidx(0, 0, zt);
+  SB_NCCL(ncclGroupStart());
+  if (sl.nranks_below) {
+    SB_NCCL(ncclSend(vb, size_t(P), ncclDouble, r - 1, comm, s));
+    SB_NCCL(ncclSend(v + sl.lidx(0, 0, zb + 1), size_t(P), ncclDouble, r - 1, comm, s));
+    SB_NCCL(ncclRecv(plane_lo.p, size_t(P), ncclDouble, r - 1, comm, s));
+    SB_NCCL(ncclRecv(v + sl.lidx(0, 0, zb - 1), size_t(P), ncclDouble, r - 1, comm, s));
+  }
+  if (sl.nranks_above) {
+    SB_NCCL(ncclSend(vt, size_t(P), ncclDouble, r + 1, comm, s));
+    SB_NCCL(ncclSend(v + sl.lidx(0, 0, zt - 1), size_t(P), ncclDouble, r + 1, comm, s));
+    SB_NCCL(ncclRecv(plane_hi.p, size_t(P), ncclDouble, r + 1, comm, s));
+    SB_NCCL(ncclRecv(v + sl.lidx(0, 0, zt + 1), size_t(P), ncclDouble, r + 1, comm, s));
+  }
+  SB_NCCL(ncclGroupEnd());
+  if (sl.nranks_below) ctx->count(launch_add_planes(vb, plane_lo.p, vb, P, s));  // lower partial first
+  if (sl.nranks_above) ctx->count(launch_add_planes(vt, vt, plane_hi.p, P, s));
+}
+
+// owner_copy_up of up to three vectors in one grouped call.
+void semlab_space_s::owner_copy_up_n(double* const* vs, int k) {
+  if (!distributed() || no_exchange()) return;
+  const int64_t P = sl.Nx * sl.Ny;
+  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+  cudaStream_t s = ctx->stream;
+  const int r = ctx->rank;
+  SB_NCCL(ncclGroupStart());
+  for (int i = 0; i < k; ++i) {
+    double* v = vs[i];
+    if (sl.nranks_above)
+      SB_NCCL(ncclSend(v + sl.lidx(0, 0, int64_t(sl.ez1) * sl.q), size_t(P), ncclDouble, r + 1, comm, s));
+    if (sl.nranks_below)
+      SB_NCCL(ncclRecv(v + sl.lidx(0, 0, int64_t(sl.ez0) * sl.q), size_t(P), ncclDouble, r - 1, comm, s));
+  }
+  SB_NCCL(ncclGroupEnd());
+}
+
 // Ghost planes z = ez0 q - 1 and z = ez1 q + 1 (the Schwarz halo, schwarz.cpp:159-168).
 void semlab_space_s::halo_exchange(double* v) {
-  if (!distributed()) return;
+  if (!distributed() || no_exchange()) return;
   const int64_t P = sl.Nx * sl.Ny;
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
   cudaStream_t s = ctx->stream;
@@ -173,7 +235,7 @@ void semlab_space_s::halo_exchange(double* v) {
 // The interface plane z = ez1 q is owned by the lower rank for owner-write operators (RAS):
 // copy it up so both ranks hold the owner's value.
 void semlab_space_s::owner_copy_up(double* v) {
-  if (!distributed()) return;
+  if (!distributed() || no_exchange()) return;
   const int64_t P = sl.Nx * sl.Ny;
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
   cudaStream_t s = ctx->stream;
