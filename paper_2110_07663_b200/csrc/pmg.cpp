@@ -425,6 +425,7 @@ static Grid3 grid_of(const Slab& sl) {
 
 semlab_pmg_s::~semlab_pmg_s() {
   if (ctx) cudaStreamSynchronize(ctx->stream);
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
   for (auto& L : lv) {
     delete L.cheb;
     delete L.A;
@@ -600,10 +601,62 @@ void semlab_pmg_s::cycle(int l) {
   L.cheb->smooth(L.b.p, L.x.p, false);
 }
 
+// SEMLAB_PMG_GRAPH=0 launches the V-cycle kernel by kernel instead of as a CUDA graph.
+static bool pmg_graph_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SEMLAB_PMG_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// The V-cycle body works on the hierarchy's own buffers only (the input and output are copied
+// in and out), so after one eager warm-up call (lazy allocations, per-kernel launch setup) it is
+// captured once as a CUDA graph, NCCL exchanges included, and replayed: one launch per cycle
+// instead of ~100, no host launch gaps between the small coarse-level kernels.
+void semlab_pmg_s::run_cycle() {
+  cudaStream_t s = ctx->stream;
+  if (!pmg_graph_enabled() || graph_state < 0) {
+    cycle(0);
+    return;
+  }
+  if (graph_state == 0) {  // eager warm-up
+    cycle(0);
+    graph_state = 1;
+    return;
+  }
+  if (graph_state == 1) {
+    const int64_t before = ctx->launches;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      try {
+        cycle(0);
+      } catch (...) {
+        ok = false;
+      }
+      ok = (cudaStreamEndCapture(s, &g) == cudaSuccess) && ok && g != nullptr;
+    }
+    if (ok) ok = cudaGraphInstantiate(&graph_exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    graph_launches = ctx->launches - before;
+    ctx->launches = before;  // the capture executed nothing
+    if (!ok) {
+      (void)cudaGetLastError();
+      graph_state = -1;  // not capturable here: stay eager
+      cycle(0);
+      return;
+    }
+    graph_state = 2;
+  }
+  SB_CUDA(cudaGraphLaunch(graph_exec, s));
+  ctx->count(graph_launches);
+}
+
 void semlab_pmg_s::vcycle(const double* b, double* z) {
   const int64_t n = lv[0].sp->n;
   ctx->count(launch_copy(lv[0].b.p, b, n, ctx->stream));
-  cycle(0);
+  run_cycle();
   ctx->count(launch_copy(z, lv[0].x.p, n, ctx->stream));
 }
 

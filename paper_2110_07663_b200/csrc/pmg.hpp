@@ -89,4 +89,8 @@ struct semlab_pmg_s {
   void restrict_(int l, const double* fine_v, double* coarse_v);
   void vcycle(const double* b, double* z);
   void cycle(int l);
+  void run_cycle();  // cycle(0), replayed as a captured CUDA graph after one eager call
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_state = 0;  // 0 not run, 1 warmed up, 2 captured, -1 eager only
+  int64_t graph_launches = 0;
 };
