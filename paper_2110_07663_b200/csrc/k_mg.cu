@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
                                               const Grid3 gout, const Jmat J, const int qf_rt, const int qc_rt,
                                               const int E_axis, const int mask_in, const Grid3 gmask_in,
                                               const int mask_out, const Grid3 gmask_out, const int zb, const int nz,
-                                              const int add_out) {
+                                              const int add_out, const double* __restrict__ sub_from) {
   const int qf = QF > 0 ? QF : qf_rt, qc = QC > 0 ? QC : qc_rt;
   const unsigned nx = unsigned(gout.N[0]), ny = unsigned(gout.N[1]);
   const unsigned total = nx * ny * unsigned(nz);
@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
     // input row through this point along AXIS; the other two coordinates fix the mask test
     int c0[3] = {c[0], c[1], c[2]};
     c0[AXIS] = 0;
-    const double* row_in = in + gin.idx(c0[0], c0[1], c0[2]);
+    const int64_t row_off = gin.idx(c0[0], c0[1], c0[2]);
+    const double* row_in = in + row_off;
+    const double* row_sub = sub_from ? sub_from + row_off : nullptr;
     bool other_bnd = false;
     if (mask_in && gmask_in.dirichlet) {
 #pragma unroll
@@ -62,7 +64,8 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
     const bool min_ = mask_in && gmask_in.dirichlet;
     auto fetch = [&](int coord) -> double {
       if (min_ && (other_bnd || coord == 0 || coord == nax_in - 1)) return 0.0;
-      return row_in[coord * sin];
+      // sub_from: the input is (sub_from - in), e.g. the residual b - A x fused into Pᵀ
+      return row_sub ? row_sub[coord * sin] - row_in[coord * sin] : row_in[coord * sin];
     };
     const int X = c[AXIS];
     double acc = 0.0;
@@ -120,7 +123,8 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
 
 int64_t launch_transfer_pass(bool prolong, const double* in, const Grid3& gin, double* out, const Grid3& gout,
                              int axis, const Jmat& J, int qf, int qc, int E_axis, bool mask_in, const Grid3& gmi,
-                             bool mask_out, const Grid3& gmo, int64_t zb, int64_t nz, cudaStream_t s, bool add_out) {
+                             bool mask_out, const Grid3& gmo, int64_t zb, int64_t nz, cudaStream_t s, bool add_out,
+                             const double* sub_from) {
   const int64_t total = gout.N[0] * gout.N[1] * nz;
   if (total <= 0) return 0;
   if (total >= (int64_t(1) << 32) || gmi.N[2] >= (int64_t(1) << 31) || zb >= (int64_t(1) << 31))
@@ -128,7 +132,7 @@ int64_t launch_transfer_pass(bool prolong, const double* in, const Grid3& gin, d
   if (axis < 0 || axis > 2) invalid("transfer pass: axis must be 0, 1 or 2");
 #define L3_(PR, AX, QF, QC)                                                                                       \
   k_pass<PR, AX, QF, QC><<<grid_for(total), 256, 0, s>>>(in, gin, out, gout, J, qf, qc, E_axis, mask_in, gmi, mask_out, \
-                                                          gmo, int(zb), int(nz), int(add_out))
+                                                          gmo, int(zb), int(nz), int(add_out), sub_from)
 #define L_(PR, AX)                                     \
   do {                                                 \
     if (qf == 7 && qc == 3) L3_(PR, AX, 7, 3);         \

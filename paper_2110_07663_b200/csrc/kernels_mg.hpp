@@ -38,7 +38,8 @@ __global__ void k_foreach_mg(int64_t n, F f) {
 int64_t launch_transfer_pass(bool prolong, const double* in, const Grid3& gin, double* out, const Grid3& gout,
                              int axis, const Jmat& J, int qf, int qc, int E_axis, bool mask_in, const Grid3& gmi,
                              bool mask_out, const Grid3& gmo, int64_t zb, int64_t nz, cudaStream_t s,
-                             bool add_out = false);  // add_out: out += pass result
+                             bool add_out = false,  // add_out: out += pass result
+                             const double* sub_from = nullptr);  // input is (sub_from - in)
 int64_t launch_gather_free(const Slab& sl, const double* full, double* freev, cudaStream_t s);
 int64_t launch_scatter_free(const Slab& sl, const double* freev, double* full, cudaStream_t s);
 int64_t launch_symv(const double* M, int64_t n, const double* x, double* y, cudaStream_t s);

@@ -549,7 +549,7 @@ void semlab_pmg_s::prolong(int l, const double* cv, double* fv, bool add) {
 }
 
 // P^T: fine level l -> coarse level l+1 (passes x, y, z)
-void semlab_pmg_s::restrict_(int l, const double* fv, double* cv) {
+void semlab_pmg_s::restrict_(int l, const double* fv, double* cv, const double* sub_from) {
   const Slab& f = lv[size_t(l)].sp->sl;
   const Slab& c = lv[size_t(l) + 1].sp->sl;
   const int qf = f.q, qc = c.q;
@@ -563,7 +563,8 @@ void semlab_pmg_s::restrict_(int l, const double* fv, double* cv) {
   g2.nyl = c.Ny;
   const int64_t zbf = int64_t(f.ez0) * qf, nzf = int64_t(f.ez1 - f.ez0) * qf + 1;
   const int64_t zbc = int64_t(c.ez0) * qc, nzc = int64_t(c.ez1 - c.ez0) * qc + 1;
-  ctx->count(launch_transfer_pass(false, fv, gf, tA.p, g1, 0, J[size_t(l)], qf, qc, f.Ex, true, gf, false, gc, zbf, nzf, s));
+  ctx->count(launch_transfer_pass(false, fv, gf, tA.p, g1, 0, J[size_t(l)], qf, qc, f.Ex, true, gf, false, gc, zbf, nzf, s,
+                                  false, sub_from));
   ctx->count(launch_transfer_pass(false, tA.p, g1, tB.p, g2, 1, J[size_t(l)], qf, qc, f.Ey, false, gf, false, gc, zbf, nzf, s));
   Jmat Jz = J[size_t(l)];
   Jz.e_lo = f.ez0;  // z: only this slab's element layers contribute; the other rank's part
@@ -586,16 +587,10 @@ void semlab_pmg_s::cycle(int l) {
   const int64_t n = L.sp->n;
   SB_CUDA(cudaMemsetAsync(L.x.p, 0, size_t(n) * sizeof(double), s));
   L.cheb->smooth(L.b.p, L.x.p, true);
-  if (L.sp->distributed()) {  // the residual needs the summed interface planes first
-    L.sp->apply_A(L.x.p, L.r.p, L.A->geom32);
-    ctx->count(launch_sub(L.r.p, L.b.p, L.r.p, n, s));
-  } else {
-    EpiArgs a;
-    a.w = L.r.p;
-    a.b = L.b.p;
-    L.sp->ax(L.x.p, Epi::Residual, a, L.A->geom32);
-  }
-  restrict_(l, L.r.p, lv[size_t(l) + 1].b.p);
+  // r = b - A x is not stored: the first restriction pass reads b and A x (bitwise the same
+  // b - Ax), so the Ax keeps the plain-write epilogue
+  L.sp->apply_A(L.x.p, L.r.p, L.A->geom32);  // (+ the interface-plane sum on a slab)
+  restrict_(l, L.r.p, lv[size_t(l) + 1].b.p, L.b.p);
   cycle(l + 1);
   prolong(l, lv[size_t(l) + 1].x.p, L.x.p, true);  // x += P e_C (fused into the last pass)
   L.cheb->smooth(L.b.p, L.x.p, false);

@@ -86,7 +86,7 @@ struct semlab_pmg_s {
   ~semlab_pmg_s();
   void build();
   void prolong(int l, const double* coarse_v, double* fine_v, bool add = false);  // add: fine_v += P coarse_v
-  void restrict_(int l, const double* fine_v, double* coarse_v);
+  void restrict_(int l, const double* fine_v, double* coarse_v, const double* sub_from = nullptr);  // Pᵀ (sub_from - fine_v) if given
   void vcycle(const double* b, double* z);
   void cycle(int l);
   void run_cycle();  // cycle(0), replayed as a captured CUDA graph after one eager call
