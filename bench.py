@@ -274,7 +274,7 @@ def run_ours(args, cfg, name):
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_summary.json")))
-        if prof.get("workload") == name and world == 1:  # captured on one GPU (whole mesh per launch)
+        if prof.get("workload") in (name, describe(name, cfg)) and world == 1:  # captured on one GPU
             traffic = prof.get("ax_dram_bytes_per_launch")
     except Exception:
         pass
@@ -299,7 +299,7 @@ def run_ours(args, cfg, name):
         ras_traffic = None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_summary.json")))
-            if prof.get("workload") == name:
+            if prof.get("workload") in (name, describe(name, cfg)):
                 ras_traffic = prof.get("ras_dram_bytes_per_launch")
         except Exception:
             pass

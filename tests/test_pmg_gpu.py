@@ -141,3 +141,40 @@ def test_pmg_invalid_schedule(ctx):
         S.Pmg(mesh, (7, 3))
     with pytest.raises(ValueError, match="strictly decreasing"):
         S.Pmg(mesh, (3, 3, 1))
+
+
+_GRAPH_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2110_07663_b200 import semlab as S
+ctx = S.Context(0)
+mesh = S.generate_kershaw(0.3, 4, ctx)
+pmg = S.Pmg(mesh, (7, 3, 1), S.RAS_SMOOTHER, 2, 0.1, 1.1, 32, S.COARSE_AMG)
+b = pmg.spaces[0].build_rhs(1)
+outs = []
+for _ in range(4):  # eager warm-up, capture + replay, replays
+    z = torch.empty_like(b)
+    pmg.vcycle(b, z)
+    outs.append(z.cpu().numpy())
+np.save(sys.argv[1], np.stack(outs))
+"""
+
+
+def test_vcycle_graph_replay_is_bitwise_eager(tmp_path):
+    """The captured CUDA-graph V-cycle (pmg.cpp run_cycle) replays exactly the eager cycle: the
+    FP32-smoother V-cycle output is bitwise identical with SEMLAB_PMG_GRAPH=1 and =0, and across
+    replays."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for g in ("1", "0"):
+        f = tmp_path / f"v{g}.npy"
+        env = dict(os.environ, SEMLAB_PMG_GRAPH=g)
+        subprocess.run([sys.executable, "-c", _GRAPH_SCRIPT % root, str(f)], check=True, env=env, timeout=600)
+        res[g] = np.load(f)
+    for k in range(4):
+        assert np.array_equal(res["1"][k], res["0"][0])
+        assert np.array_equal(res["0"][k], res["0"][0])
