@@ -121,6 +121,27 @@ int ref_schwarz_apply(double eps, int E, int p, int mode, const double* r, doubl
   });
 }
 
+// Neumann mode (sem_space.hpp:12, 28): apply_A with mean removal (sem_space.cpp:207), the
+// unmasked diagonal (sem_space.cpp:211-236) and RAS/ASM with Neumann faces (schwarz.cpp:151-160).
+int ref_neumann(double eps, int E, int p, const double* u, double* Au, double* diag, const double* r,
+                double* ras, double* asm_) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p, BcMode::Neumann);
+    const size_t n = size_t(s.n());
+    FieldVector uv = Eigen::Map<const Eigen::MatrixXd>(u, s.n(), 1);
+    FieldVector w = s.apply_A(uv);
+    std::memcpy(Au, w.data(), sizeof(double) * n);
+    FieldVector d = s.stiffness_diag();
+    std::memcpy(diag, d.data(), sizeof(double) * n);
+    FieldVector rv = Eigen::Map<const Eigen::MatrixXd>(r, s.n(), 1);
+    SchwarzSmoother sr(s, SchwarzMode::Ras), sa(s, SchwarzMode::Asm);
+    FieldVector zr = sr.apply(rv), za = sa.apply(rv);
+    std::memcpy(ras, zr.data(), sizeof(double) * n);
+    std::memcpy(asm_, za.data(), sizeof(double) * n);
+  });
+}
+
 int ref_lambda(double eps, int E, int p, int smoother, double* value, int* rounds) {
   return guard([&] {
     HexMesh m = mesh_of(eps, E, p);

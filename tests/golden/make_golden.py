@@ -25,6 +25,7 @@ SOLVE_CASES = [  # (name, eps, E, orders, precond, coarse, krylov)
     ("pmg_ras_gmres_kershaw", 0.3, 4, (7, 3, 1), "ras", "direct", 0),
     ("pmg_ras_gmres_kershaw_amg", 0.3, 4, (7, 3, 1), "ras", "amg", 0),
 ]
+NEUMANN_CASES = [(0.3, 2, 5), (1.0, 4, 3)]
 
 
 def main():
@@ -87,6 +88,17 @@ def main():
         chk(lib.ref_vcycle(C.c_double(eps), E, arr, len(orders), sm.encode(), coarse.encode(), 2,
                            b.ctypes.data_as(pd), z.ctypes.data_as(pd), lams.ctypes.data_as(pd)))
         out[key], out[key + "_lams"] = z, lams
+    for eps, E, p in NEUMANN_CASES:
+        key = f"neu_e{eps}_E{E}_p{p}"
+        n = (E * p + 1) ** 3
+        rng = np.random.default_rng(7000 + 10 * p + E)
+        uu, r = rng.standard_normal(n), rng.standard_normal(n)
+        Au, diag, ras, asm = (np.zeros(n) for _ in range(4))
+        chk(lib.ref_neumann(C.c_double(eps), E, p, uu.ctypes.data_as(pd), Au.ctypes.data_as(pd),
+                            diag.ctypes.data_as(pd), r.ctypes.data_as(pd), ras.ctypes.data_as(pd),
+                            asm.ctypes.data_as(pd)))
+        out[f"{key}_u"], out[f"{key}_Au"], out[f"{key}_diag"] = uu, Au, diag
+        out[f"{key}_r"], out[f"{key}_ras"], out[f"{key}_asm"] = r, ras, asm
     for name, eps, E, orders, pc, coarse, kr in SOLVE_CASES:
         n = (E * orders[0] + 1) ** 3
         x, hist = np.zeros(n), np.zeros(500)

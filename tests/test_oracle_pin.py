@@ -88,3 +88,14 @@ def test_solves_pinned(name, eps, orders, pc, coarse, kr):
     st = o.gmres_solve(s.apply_A, M, b, x, o.GmresConfig()) if kr == 0 else o.pcg_solve(s.apply_A, M, b, x, 1e-8, 500)
     assert abs(st.iterations - int(G[f"solve_{name}_iters"][0])) <= 1
     assert rel(x, G[f"solve_{name}_x"]) < 1e-10
+
+
+@pytest.mark.parametrize("eps,E,p", [(0.3, 2, 5), (1.0, 4, 3)])
+def test_neumann_pinned(eps, E, p):
+    """Neumann mode against the reference (ref_neumann: sem_space.cpp:207, 211-236; schwarz.cpp:151-160)."""
+    key = f"neu_e{eps}_E{E}_p{p}"
+    s = o.SemSpace(o.generate_kershaw(eps, E), p, o.NEUMANN)
+    assert rel(s.apply_A(G[f"{key}_u"]), G[f"{key}_Au"]) < 1e-12
+    assert rel(s.stiffness_diag(), G[f"{key}_diag"]) < 1e-12
+    for mode, name in ((o.RAS, "ras"), (o.ASM, "asm")):
+        assert rel(o.SchwarzSmoother(s, mode).apply(G[f"{key}_r"]), G[f"{key}_{name}"]) < 1e-12

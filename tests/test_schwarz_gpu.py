@@ -93,3 +93,27 @@ def test_chebyshev_ras_fused(ctx, precision, x0_zero):
     cg.smooth(g.to_device(b), xg)
     co.smooth(b, x)
     assert rel(xg, x) < (1e-11 if precision == 64 else 1e-5)
+
+
+@pytest.mark.parametrize("eps,E,p", [(0.3, 2, 5), (1.0, 4, 3)])
+@pytest.mark.parametrize("mode", [o.RAS, o.ASM])
+def test_schwarz_neumann_fp64_matches_oracle(ctx, eps, E, p, mode):
+    """Neumann boundary sides keep the face dof (schwarz.cpp:151-160): n = p+1 at the domain
+    boundary instead of p-1, and no lattice point is masked."""
+    from paper_2110_07663_b200 import semlab as S
+    g = S.SemSpace(S.generate_kershaw(eps, E, ctx), p, S.NEUMANN)
+    c = o.SemSpace(o.generate_kershaw(eps, E), p, o.NEUMANN)
+    sg, so = S.SchwarzSmoother(g, mode, 64), o.SchwarzSmoother(c, mode, 64)
+    for e in (0, c.E - 1):
+        _, n, _ = sg.element_info(e)
+        np.testing.assert_array_equal(n, so.n[e])
+    r = np.random.default_rng(p).standard_normal(c.n)
+    assert rel(sg.apply(r), so.apply(r)) < 1e-12
+    np.testing.assert_allclose(g.stiffness_diag().cpu().numpy(), c.stiffness_diag(), rtol=1e-12)
+    # and against the reference's own Neumann outputs (tests/golden, ref_neumann)
+    import os
+    G = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_golden.npz"))
+    key = f"neu_e{eps}_E{E}_p{p}"
+    name = "ras" if mode == o.RAS else "asm"
+    assert rel(sg.apply(G[f"{key}_r"]), G[f"{key}_{name}"]) < 1e-12
+    assert rel(g.apply_A(G[f"{key}_u"]), G[f"{key}_Au"]) < 1e-12
