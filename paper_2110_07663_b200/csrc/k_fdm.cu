@@ -311,7 +311,9 @@ __global__ void __launch_bounds__(128, ras_minb<P, T>()) k_ras(const Slab sl, co
   fdm_block<P, T, false>(sl, S, L, r, e_first, nE, smem, bx);
   // owner write: sites flattened with a (x) fastest so a warp's accesses are contiguous runs;
   // U sites per thread per round with every vector load issued before any use
-  constexpr int Q = P - 3, Q3 = Q * Q * Q, U = 4;  // at most Q owned sites per direction
+  // at most q owned sites per direction, q + 1 at a Neumann domain face (its face node is kept)
+  constexpr int U = 4;
+  const int Q = sl.dirichlet ? P - 3 : P - 2, Q3 = Q * Q * Q;
   for (int base = threadIdx.x; base < EPC * Q3; base += Sh::NT * U) {
     int64_t g[U];
     bool ok[U];

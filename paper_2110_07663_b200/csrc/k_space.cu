@@ -753,6 +753,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SEMLAB_AXW_MINB
 #define SEMLAB_AXW_MINB (SEMLAB_AXW_TMA ? 5 : 3)  // resident CTAs per SM
 #endif
+#ifndef SEMLAB_AXW_MINB_F
+#define SEMLAB_AXW_MINB_F SEMLAB_AXW_MINB  // the same for the FP32-factor (smoother) operator
+#endif
 
 template <class GT>
 __host__ __device__ constexpr int axw_warp_doubles() {  // per-warp shared memory in doubles
@@ -774,7 +777,7 @@ __device__ __forceinline__ double2 ld_geom2_smem(const float* p) {
 // GT = double: the operator itself (Krylov A). GT = float: the smoother's operator with the
 // geometric factors rounded to FP32 (half the bytes; arithmetic stays FP64 on the DMMA path).
 template <class EpiT, class GT>
-__global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
+__global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLAB_AXW_MINB_F : SEMLAB_AXW_MINB)
     k_axw(const Slab sl, const DMat<8> Dm, const double* __restrict__ u, const GT* __restrict__ geom,
           double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int total_tickets,
           const EpiT epi) {

@@ -29,6 +29,36 @@ def _ptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
 
+def _own(obj, handle, destroy, *parents):
+    """Record obj's native handle in a box its parents also list. A cycle of garbage is finalised
+    in arbitrary order, so releasing a parent first releases every child box still live: handles
+    are always destroyed child-before-parent (objects.hpp: smoother -> space -> mesh -> context)."""
+    box = [handle, destroy, []]
+    obj._box = box
+    for par in parents:
+        pb = getattr(par, "_box", None)
+        if pb is not None:
+            pb[2][:] = [c for c in pb[2] if c[0]]
+            pb[2].append(box)
+
+
+def _release(obj):
+    box = getattr(obj, "_box", None)
+    if box is not None and box[0]:
+        for child in box[2]:
+            _release_box(child)
+        _release_box(box)
+    obj.handle = None
+
+
+def _release_box(box):
+    if box[0]:
+        for child in box[2]:
+            _release_box(child)
+        h, box[0] = box[0], None
+        box[1](h)
+
+
 class Context:
     """Device + stream (+ NCCL communicator). One per process and GPU."""
 
@@ -48,6 +78,7 @@ class Context:
             buf = C.create_string_buffer(nccl_id, 128)
             check(lib.semlab_ctx_create_dist(device, C.c_void_p(stream.cuda_stream), rank, nranks, buf, C.byref(h)))
         self.handle = h
+        _own(self, h, lib.semlab_ctx_destroy)
         self.rank, self.nranks = rank, nranks
 
     @staticmethod
@@ -64,9 +95,7 @@ class Context:
         return int(lib.semlab_ctx_launch_count(self.handle))
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            lib.semlab_ctx_destroy(self.handle)
-            self.handle = None
+        _release(self)
 
 
 _DEFAULT: Context | None = None
@@ -84,6 +113,7 @@ class HexMesh:
 
     def __init__(self, handle, ctx: Context, dims, keep=None):
         self.handle, self.ctx, self.dims, self._keep = handle, ctx, tuple(dims), keep
+        _own(self, handle, lib.semlab_mesh_destroy, ctx)
 
     @classmethod
     def kershaw(cls, eps: float, elements_per_axis: int, ctx: Context | None = None):
@@ -121,9 +151,7 @@ class HexMesh:
         return out.reshape(n, 3)
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            lib.semlab_mesh_destroy(self.handle)
-            self.handle = None
+        _release(self)
 
 
 def generate_kershaw(eps: float, elements_per_axis: int, ctx: Context | None = None) -> HexMesh:
@@ -136,6 +164,7 @@ class LinOp:
 
     def __init__(self, handle, n: int, ctx: Context, keep=None):
         self.handle, self.n, self.ctx, self._keep = handle, n, ctx, keep
+        _own(self, handle, lib.semlab_op_destroy, ctx, keep)
 
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
@@ -159,9 +188,7 @@ class LinOp:
         return cls(h, n, ctx, keep=cb)
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            lib.semlab_op_destroy(self.handle)
-            self.handle = None
+        _release(self)
 
 
 def _wrap_device(ptr: int, n: int, ctx: Context) -> torch.Tensor:
@@ -180,6 +207,7 @@ class SemSpace:
         h = C.c_void_p()
         check(lib.semlab_space_create(mesh.handle, int(order), int(bc), C.byref(h)))
         self.handle = h
+        _own(self, h, lib.semlab_space_destroy, mesh)
         s = (C.c_int64 * 11)()
         check(lib.semlab_space_sizes(h, s))
         (self.n, self.n_free, self.n_local_total, nx, ny, nz, self.n_global, self.n_elements,
@@ -270,9 +298,7 @@ class SemSpace:
         return LinOp(h, self.n, self.ctx, keep=self)
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            lib.semlab_space_destroy(self.handle)
-            self.handle = None
+        _release(self)
 
 
 class SchwarzSmoother:
@@ -283,6 +309,7 @@ class SchwarzSmoother:
         h = C.c_void_p()
         check(lib.semlab_schwarz_create(space.handle, int(mode), int(precision), C.byref(h)))
         self.handle = h
+        _own(self, h, lib.semlab_schwarz_destroy, space)
         self.box = space.order + 3
 
     def apply(self, r, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -310,9 +337,7 @@ class SchwarzSmoother:
         return LinOp(h, self.space.n, self.space.ctx, keep=self)
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            lib.semlab_schwarz_destroy(self.handle)
-            self.handle = None
+        _release(self)
 
 
 @dataclass
@@ -346,15 +371,14 @@ class ChebyshevSmoother:
         h = C.c_void_p()
         check(lib.semlab_cheby_create(S.handle, A.handle, C.byref(cp), C.byref(h)))
         self.handle = h
+        _own(self, h, lib.semlab_cheby_destroy, S, A)
 
     def smooth(self, b: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
         check(lib.semlab_cheby_smooth(self.handle, _ptr(b), _ptr(x)))
         return x
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            lib.semlab_cheby_destroy(self.handle)
-            self.handle = None
+        _release(self)
 
 
 class Pmg:
@@ -368,11 +392,13 @@ class Pmg:
         check(lib.semlab_pmg_create(mesh.handle, len(orders), arr, int(smoother), int(cheb_order), float(lmin_mult),
                                     float(lmax_mult), int(precision), int(coarse), C.byref(h)))
         self.handle = h
+        _own(self, h, lib.semlab_pmg_destroy, mesh)
         self.spaces = []
         for lvl in range(len(orders)):
             sh = C.c_void_p()
             check(lib.semlab_pmg_space(h, lvl, C.byref(sh)))
             self.spaces.append(_BorrowedSpace(sh, mesh, orders[lvl]))
+            self.spaces[-1]._box = self._box  # smoothers built on a level are children of the hierarchy
         self.n = self.spaces[0].n
 
     def lam(self, level: int) -> float:
@@ -401,9 +427,7 @@ class Pmg:
         return LinOp(h, self.n, self.mesh.ctx, keep=self)
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            lib.semlab_pmg_destroy(self.handle)
-            self.handle = None
+        _release(self)
 
 
 class _BorrowedSpace(SemSpace):

@@ -228,3 +228,23 @@ def test_oracle_gmres_identity_one_iteration():
     st = o.gmres_solve(lambda v: v.copy(), None, b, x, o.GmresConfig())
     assert st.converged and st.iterations == 1
     np.testing.assert_allclose(x, b, atol=1e-14)
+
+
+def test_handles_released_child_first_in_any_finalisation_order():
+    """A garbage cycle is finalised in arbitrary order; native handles must still be destroyed
+    child-before-parent (a smoother's destroy reads its space's context)."""
+    from paper_2110_07663_b200 import semlab as S
+    log = []
+
+    class Obj:
+        pass
+
+    ctx, mesh, space, sch = Obj(), Obj(), Obj(), Obj()
+    S._own(ctx, 1, lambda h: log.append(("ctx", h)))
+    S._own(mesh, 2, lambda h: log.append(("mesh", h)), ctx)
+    S._own(space, 3, lambda h: log.append(("space", h)), mesh)
+    S._own(sch, 4, lambda h: log.append(("sch", h)), space)
+    for obj in (ctx, space, sch, mesh):  # parent finalised first
+        S._release(obj)
+    assert log == [("sch", 4), ("space", 3), ("mesh", 2), ("ctx", 1)]
+    assert all(o.handle is None for o in (ctx, mesh, space, sch))

@@ -117,3 +117,16 @@ def test_schwarz_neumann_fp64_matches_oracle(ctx, eps, E, p, mode):
     name = "ras" if mode == o.RAS else "asm"
     assert rel(sg.apply(G[f"{key}_r"]), G[f"{key}_{name}"]) < 1e-12
     assert rel(g.apply_A(G[f"{key}_u"]), G[f"{key}_Au"]) < 1e-12
+
+
+@pytest.mark.parametrize("mode", [o.RAS, o.ASM])
+def test_schwarz_neumann_fp32(ctx, mode):
+    """The paper's FP32 smoother (warp-per-element RAS at p=7) in Neumann mode: the first element
+    along each axis owns q + 1 sites."""
+    from paper_2110_07663_b200 import semlab as S
+    g = S.SemSpace(S.generate_kershaw(0.3, 4, ctx), 7, S.NEUMANN)
+    c = o.SemSpace(o.generate_kershaw(0.3, 4), 7, o.NEUMANN)
+    r = np.random.default_rng(3).standard_normal(c.n)
+    z = S.SchwarzSmoother(g, mode, 32).apply(r)
+    assert rel(z, o.SchwarzSmoother(c, mode, 64).apply(r)) < 2e-5
+    assert rel(z, o.SchwarzSmoother(c, mode, 32).apply(r)) < 2e-6
