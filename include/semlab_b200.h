@@ -42,6 +42,7 @@ typedef struct semlab_space_s* semlab_space;     /* SemSpace, sem_space.hpp:26-1
 typedef struct semlab_schwarz_s* semlab_schwarz; /* SchwarzSmoother, schwarz.hpp:31-86     */
 typedef struct semlab_op_s* semlab_op;           /* LinOp, types.hpp:13                    */
 typedef struct semlab_cheby_s* semlab_cheby;     /* ChebyshevSmoother, chebyshev.hpp:36-46 */
+typedef struct semlab_proj_s* semlab_proj;       /* ProjectionBasis, krylov.hpp:39-59      */
 typedef struct semlab_pmg_s* semlab_pmg;         /* pMG hierarchy (pmg.cpp is MISSING in the
                                                     reference; API of SPEC.md:313-349)     */
 
@@ -207,6 +208,21 @@ int semlab_gmres_solve(semlab_op A, semlab_op M, const double* d_b, double* d_x,
    ignored; converges on ||r|| <= tol ||b - A x0||. */
 int semlab_pcg_solve(semlab_op A, semlab_op M, const double* d_b, double* d_x,
                      const semlab_gmres_config* config, semlab_gmres_stats* stats);
+
+/* ---- ProjectionBasis (krylov.hpp:35-59, krylov.cpp:131-152) ------------------------------
+   A-orthonormal basis of prior solutions kept on the device (vectors of length n of the
+   operator's space). capacity in [1, 24]. */
+int semlab_proj_create(semlab_ctx ctx, int64_t n, int capacity, semlab_proj* out);
+int semlab_proj_destroy(semlab_proj p);
+/* u = sum_i (x_i . b) x_i, zero for an empty basis (ProjectionBasis::initial_guess). */
+int semlab_proj_initial_guess(semlab_proj p, const double* d_b, double* d_u);
+/* A-orthonormalise x into the basis, two classical passes, skip if dependent, evict the oldest
+   beyond capacity (ProjectionBasis::insert). A must act on vectors of length n. */
+int semlab_proj_insert(semlab_proj p, const double* d_x, semlab_op A);
+int semlab_proj_size(semlab_proj p, int* out);
+int semlab_proj_clear(semlab_proj p);
+/* basis vector i (0 = oldest) copied to d_out */
+int semlab_proj_vector(semlab_proj p, int i, double* d_out);
 
 /* ---- host-only helpers (no GPU needed; used by the CPU test suite) ------------------------ */
 /* gll(order), gll.cpp:80-91: nodes, weights (order+1) and diff (column-major (order+1)^2). */

@@ -142,6 +142,29 @@ int ref_neumann(double eps, int E, int p, const double* u, double* Au, double* d
   });
 }
 
+// ProjectionBasis (krylov.cpp:131-152): insert the K columns of X (n x K, column-major) one by
+// one with A = apply_A of the space, then return the basis (oldest first) and the projected
+// guess for b.
+int ref_projection(double eps, int E, int p, int capacity, int K, const double* X, const double* b,
+                   int* size, double* basis, double* guess) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    LinOp A = [&s](const FieldVector& in, FieldVector& out) { out = s.apply_A(in); };
+    ProjectionBasis pb(capacity);
+    const size_t n = size_t(s.n());
+    for (int k = 0; k < K; ++k) {
+      FieldVector x = Eigen::Map<const Eigen::MatrixXd>(X + n * size_t(k), s.n(), 1);
+      pb.insert(x, A);
+    }
+    *size = pb.size();
+    for (int i = 0; i < pb.size(); ++i) std::memcpy(basis + n * size_t(i), pb.vectors()[size_t(i)].data(), 8 * n);
+    FieldVector bv = Eigen::Map<const Eigen::MatrixXd>(b, s.n(), 1);
+    FieldVector u = pb.initial_guess(bv);
+    std::memcpy(guess, u.data(), 8 * n);
+  });
+}
+
 int ref_lambda(double eps, int E, int p, int smoother, double* value, int* rounds) {
   return guard([&] {
     HexMesh m = mesh_of(eps, E, p);

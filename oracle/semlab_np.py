@@ -821,6 +821,36 @@ def gmres_solve(A, M, b, x, config: GmresConfig) -> GmresStats:
     return st
 
 
+class ProjectionBasis:
+    """krylov.hpp:39-59 / krylov.cpp:131-152: A-orthonormal prior solutions, oldest first."""
+
+    def __init__(self, capacity=10):
+        self.capacity, self.basis = capacity, []
+
+    def initial_guess(self, b):
+        u = np.zeros_like(b)
+        for v in self.basis:  # krylov.cpp:134-137
+            u += v.dot(b) * v
+        return u
+
+    def insert(self, x, A):
+        if A is None:
+            raise ValueError("ProjectionBasis: missing operator")
+        w = x.copy()
+        aw = A(w)
+        norm0 = np.sqrt(max(0.0, w.dot(aw)))
+        for _ in range(2):  # krylov.cpp:144-147: coefficients from the same A w within a pass
+            for v in self.basis:
+                w -= v.dot(aw) * v
+            aw = A(w)
+        norm = np.sqrt(max(0.0, w.dot(aw)))
+        if not norm > 1e-12 * max(norm0, 1e-300):
+            return
+        self.basis.append(w / norm)
+        if len(self.basis) > self.capacity:
+            self.basis.pop(0)
+
+
 @dataclass
 class PcgStats:
     iterations: int = 0

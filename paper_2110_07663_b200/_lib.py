@@ -105,6 +105,13 @@ SIGNATURES = {
     "semlab_pmg_restrict": (i32, [p, i32, p, p]),
     "semlab_gmres_solve": (i32, [p, p, p, p, C.POINTER(GmresConfigC), C.POINTER(GmresStatsC)]),
     "semlab_pcg_solve": (i32, [p, p, p, p, C.POINTER(GmresConfigC), C.POINTER(GmresStatsC)]),
+    "semlab_proj_create": (i32, [p, i64, i32, C.POINTER(p)]),
+    "semlab_proj_destroy": (i32, [p]),
+    "semlab_proj_initial_guess": (i32, [p, p, p]),
+    "semlab_proj_insert": (i32, [p, p, p]),
+    "semlab_proj_size": (i32, [p, C.POINTER(i32)]),
+    "semlab_proj_clear": (i32, [p]),
+    "semlab_proj_vector": (i32, [p, i32, p]),
     "semlab_host_gll": (i32, [i32, pf64, pf64, pf64]),
     "semlab_host_kershaw_map": (i32, [f64, f64, f64, f64, pf64]),
     "semlab_host_uniform_pm1": (i32, [u64, i64, pf64]),

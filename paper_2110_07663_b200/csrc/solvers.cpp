@@ -9,7 +9,10 @@
 #include <cstdlib>
 
 #include "host_math.hpp"
+#include "capi_util.hpp"
 #include "schwarz.hpp"
+
+#include <memory>
 
 using namespace sb;
 
@@ -489,3 +492,121 @@ KrylovResult pcg_solve(semlab_op A, semlab_op M, const double* b, double* x, con
 }
 
 }  // namespace sb
+
+// ------------------------------------------------------------------------------ ProjectionBasis
+// krylov.cpp:131-152. The basis is column-major with 256-byte aligned columns, oldest first,
+// plus one spare column that receives a new vector before the oldest is evicted.
+void semlab_proj_s::init(semlab_ctx c, int64_t n_, int cap) {
+  if (!c) invalid("ProjectionBasis: missing context");
+  if (n_ < 1) invalid("ProjectionBasis: n must be >= 1");
+  if (cap < 1 || cap > 24) invalid("ProjectionBasis: capacity must be in [1, 24] on the device path");
+  ctx = c;
+  n = n_;
+  own = {n_, 0, n_};
+  capacity = cap;
+  ld = padded(n_);
+  V.alloc(size_t(ld) * (cap + 1));
+  w.alloc(size_t(n_));
+  aw.alloc(size_t(n_));
+  dh.alloc(96);
+}
+
+void semlab_proj_s::initial_guess(const double* b, double* u) {
+  cudaStream_t s = ctx->stream;
+  const OwnRange& o = own;
+  if (size == 0) {
+    ctx->count(launch_fill(u, n, 0.0, s));
+    return;
+  }
+  std::vector<double> h(static_cast<size_t>(size));
+  ctx->count(launch_gemv_t(V.p, ld, size, b, o.off, o.len, dh.p, ctx->dots(), s));
+  fetch(ctx, dh.p, h.data(), size);
+  ctx->count(launch_gemv_n(V.p, ld, size, h.data(), u, n, s));
+}
+
+void semlab_proj_s::insert(const double* x, semlab_op A) {
+  if (!A) invalid("ProjectionBasis: missing operator");
+  if (A->n != n) invalid("ProjectionBasis: operator size differs from the basis length");
+  cudaStream_t s = ctx->stream;
+  const OwnRange o = own_range_of(A);
+  own = o;
+  SB_CUDA(cudaMemcpyAsync(w.p, x, sizeof(double) * size_t(n), cudaMemcpyDeviceToDevice, s));
+  A->apply(w.p, aw.p);
+  const double* a[1] = {w.p};
+  const double* b[1] = {aw.p};
+  double wa = 0.0;
+  ctx->dots(1, a, b, o.off, o.len, &wa);
+  const double norm0 = std::sqrt(std::max(0.0, wa));
+  if (size > 0) {
+    for (int pass = 0; pass < 2; ++pass) {  // w -= sum_i (x_i . Aw) x_i with Aw fixed per pass
+      ctx->count(launch_gemv_t(V.p, ld, size, aw.p, o.off, o.len, dh.p, ctx->dots(), s));
+      ctx->allreduce_device(dh.p, size);
+      ctx->count(launch_cgs_update_norm(V.p, ld, size, w.p, dh.p, n, o.off, o.len, dh.p + 64, ctx->dots(), s));
+      A->apply(w.p, aw.p);
+    }
+  }
+  ctx->dots(1, a, b, o.off, o.len, &wa);
+  const double norm = std::sqrt(std::max(0.0, wa));
+  if (!(norm > 1e-12 * std::max(norm0, 1e-300))) return;  // numerically dependent
+  ctx->count(launch_div(V.p + size_t(ld) * size, w.p, norm, n, s));
+  if (++size > capacity) {  // evict the oldest: shift columns down (non-overlapping copies)
+    for (int k = 0; k < capacity; ++k)
+      SB_CUDA(cudaMemcpyAsync(V.p + size_t(ld) * k, V.p + size_t(ld) * (k + 1), sizeof(double) * size_t(n),
+                              cudaMemcpyDeviceToDevice, s));
+    size = capacity;
+  }
+}
+
+int semlab_proj_create(semlab_ctx ctx, int64_t n, int capacity, semlab_proj* out) {
+  return guard([&] {
+    need(out, "ProjectionBasis: out");
+    auto p = std::make_unique<semlab_proj_s>();
+    p->init(ctx, n, capacity);
+    *out = p.release();
+  });
+}
+
+int semlab_proj_destroy(semlab_proj p) {
+  return guard([&] {
+    if (p) cudaStreamSynchronize(p->ctx->stream);
+    delete p;
+  });
+}
+
+int semlab_proj_initial_guess(semlab_proj p, const double* b, double* u) {
+  return guard([&] {
+    need(p, "ProjectionBasis: basis");
+    p->initial_guess(b, u);
+  });
+}
+
+int semlab_proj_insert(semlab_proj p, const double* x, semlab_op A) {
+  return guard([&] {
+    need(p, "ProjectionBasis: basis");
+    p->insert(x, A);
+  });
+}
+
+int semlab_proj_size(semlab_proj p, int* out) {
+  return guard([&] {
+    need(p, "ProjectionBasis: basis");
+    need(out, "ProjectionBasis: out");
+    *out = p->size;
+  });
+}
+
+int semlab_proj_clear(semlab_proj p) {
+  return guard([&] {
+    need(p, "ProjectionBasis: basis");
+    p->size = 0;
+  });
+}
+
+int semlab_proj_vector(semlab_proj p, int i, double* out) {
+  return guard([&] {
+    need(p, "ProjectionBasis: basis");
+    if (i < 0 || i >= p->size) invalid("ProjectionBasis: vector index out of range");
+    SB_CUDA(cudaMemcpyAsync(out, p->V.p + size_t(p->ld) * i, sizeof(double) * size_t(p->n),
+                            cudaMemcpyDeviceToDevice, p->ctx->stream));
+  });
+}

@@ -36,3 +36,15 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
 KrylovResult pcg_solve(semlab_op A, semlab_op M, const double* b, double* x, const semlab_gmres_config& cfg);
 
 }  // namespace sb
+
+// ProjectionBasis (krylov.hpp:39-59) over device vectors.
+struct semlab_proj_s {
+  semlab_ctx ctx = nullptr;
+  int64_t n = 0, ld = 0;
+  int capacity = 0, size = 0;
+  sb::OwnRange own{0, 0, 0};  // reduction range of the operator last inserted with
+  sb::DevBuf<double> V, w, aw, dh;
+  void init(semlab_ctx c, int64_t n_, int cap);
+  void initial_guess(const double* b, double* u);
+  void insert(const double* x, semlab_op A);
+};

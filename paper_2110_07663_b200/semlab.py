@@ -491,6 +491,61 @@ def pcg_solve(A: LinOp, M: LinOp | None, b: torch.Tensor, x: torch.Tensor, confi
 
 
 # ---- host-only helpers --------------------------------------------------------------------------
+class ProjectionBasis:
+    """ProjectionBasis(capacity), krylov.hpp:39-59: A-orthonormal prior solutions on the device.
+    n is the vector length of the operator's space (fixed at the first use)."""
+
+    def __init__(self, capacity: int = 10, n: int | None = None, ctx: Context | None = None):
+        self.capacity, self.n, self.ctx = int(capacity), n, ctx
+        self.handle = None
+        if n is not None:
+            self._create(n, ctx)
+
+    def _create(self, n: int, ctx: Context | None):
+        self.ctx = ctx or self.ctx or default_context()
+        self.n = int(n)
+        h = C.c_void_p()
+        check(lib.semlab_proj_create(self.ctx.handle, self.n, self.capacity, C.byref(h)))
+        self.handle = h
+        _own(self, h, lib.semlab_proj_destroy, self.ctx)
+
+    def initial_guess(self, b: torch.Tensor) -> torch.Tensor:
+        u = torch.zeros_like(b)
+        if self.handle is None:
+            return u
+        check(lib.semlab_proj_initial_guess(self.handle, _ptr(b), _ptr(u)))
+        return u
+
+    def insert(self, x: torch.Tensor, A: LinOp) -> None:
+        if A is None:
+            raise ValueError("ProjectionBasis: missing operator")
+        if self.handle is None:
+            self._create(A.n, A.ctx)
+        check(lib.semlab_proj_insert(self.handle, _ptr(x), A.handle))
+
+    def size(self) -> int:
+        if self.handle is None:
+            return 0
+        v = C.c_int()
+        check(lib.semlab_proj_size(self.handle, C.byref(v)))
+        return v.value
+
+    def vectors(self) -> list:
+        out = []
+        for i in range(self.size()):
+            v = torch.empty(self.n, dtype=torch.float64, device=self.ctx.torch_device)
+            check(lib.semlab_proj_vector(self.handle, i, _ptr(v)))
+            out.append(v)
+        return out
+
+    def clear(self) -> None:
+        if self.handle is not None:
+            check(lib.semlab_proj_clear(self.handle))
+
+    def __del__(self):
+        _release(self)
+
+
 def host_gll(order: int):
     n = order + 1
     nodes, w, d = np.zeros(n), np.zeros(n), np.zeros(n * n)

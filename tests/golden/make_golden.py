@@ -99,6 +99,21 @@ def main():
                             asm.ctypes.data_as(pd)))
         out[f"{key}_u"], out[f"{key}_Au"], out[f"{key}_diag"] = uu, Au, diag
         out[f"{key}_r"], out[f"{key}_ras"], out[f"{key}_asm"] = r, ras, asm
+    # ProjectionBasis: capacity 3, six inserts. The 4th repeats the 2nd (dependent: skipped);
+    # the 5th and 6th evict the two oldest.
+    eps, E, p = 0.3, 2, 4
+    n = (E * p + 1) ** 3
+    rng = np.random.default_rng(4242)
+    X = rng.standard_normal((6, n))
+    X[3] = X[1]  # dependent on the basis: skipped
+    b = rng.standard_normal(n)
+    Xc = np.ascontiguousarray(X)
+    size = C.c_int()
+    basis, guess = np.zeros((3, n)), np.zeros(n)
+    chk(lib.ref_projection(C.c_double(eps), E, p, 3, 6, Xc.ctypes.data_as(pd), b.ctypes.data_as(pd),
+                           C.byref(size), basis.ctypes.data_as(pd), guess.ctypes.data_as(pd)))
+    out["proj_X"], out["proj_b"], out["proj_size"] = X, b, np.array([size.value])
+    out["proj_basis"], out["proj_guess"] = basis[:size.value], guess
     for name, eps, E, orders, pc, coarse, kr in SOLVE_CASES:
         n = (E * orders[0] + 1) ** 3
         x, hist = np.zeros(n), np.zeros(500)

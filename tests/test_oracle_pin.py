@@ -99,3 +99,19 @@ def test_neumann_pinned(eps, E, p):
     assert rel(s.stiffness_diag(), G[f"{key}_diag"]) < 1e-12
     for mode, name in ((o.RAS, "ras"), (o.ASM, "asm")):
         assert rel(o.SchwarzSmoother(s, mode).apply(G[f"{key}_r"]), G[f"{key}_{name}"]) < 1e-12
+
+
+def test_projection_basis_pinned():
+    """ProjectionBasis (krylov.cpp:131-152) against the reference: skip of a dependent vector,
+    eviction of the oldest, A-orthonormality and the projected guess."""
+    s = o.SemSpace(o.generate_kershaw(0.3, 2), 4)
+    pb = o.ProjectionBasis(3)
+    for x in G["proj_X"]:
+        pb.insert(x, s.apply_A)
+    assert len(pb.basis) == int(G["proj_size"][0]) == 3
+    for v, ref in zip(pb.basis, G["proj_basis"]):
+        assert rel(v, ref) < 1e-11
+    assert rel(pb.initial_guess(G["proj_b"]), G["proj_guess"]) < 1e-11
+    Vb = np.stack(pb.basis, axis=1)
+    gram = Vb.T @ np.stack([s.apply_A(v) for v in pb.basis], axis=1)
+    assert np.abs(gram - np.eye(3)).max() < 1e-12
