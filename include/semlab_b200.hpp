@@ -225,6 +225,35 @@ class ChebyshevSmoother {  // chebyshev.hpp:36-46
   semlab_cheby h_ = nullptr;
 };
 
+// ProjectionBasis, krylov.hpp:39-59. The device basis needs its context and vector length up
+// front (the reference sizes it from the first inserted vector).
+class ProjectionBasis {
+ public:
+  ProjectionBasis(const Context& ctx, Index n, int capacity = 10) : capacity_(capacity) {
+    check(semlab_proj_create(ctx.handle(), n, capacity, &h_));
+  }
+  ~ProjectionBasis() { semlab_proj_destroy(h_); }
+  ProjectionBasis(const ProjectionBasis&) = delete;
+  void initial_guess(const DeviceVector& b, DeviceVector& u) const {
+    check(semlab_proj_initial_guess(h_, b.data(), u.data()));
+  }
+  void insert(const DeviceVector& x, const LinOp& A) {
+    if (!A) throw std::invalid_argument("ProjectionBasis: missing operator");
+    check(semlab_proj_insert(h_, x.data(), A.handle()));
+  }
+  int size() const {
+    int k = 0;
+    check(semlab_proj_size(h_, &k));
+    return k;
+  }
+  int capacity() const { return capacity_; }
+  void clear() { check(semlab_proj_clear(h_)); }
+
+ private:
+  semlab_proj h_ = nullptr;
+  int capacity_;
+};
+
 class Pmg {  // pMG V-cycle (pmg.cpp missing in the reference)
  public:
   Pmg(std::shared_ptr<HexMesh> mesh, std::vector<int> orders, int smoother = SEMLAB_SMOOTHER_RAS, int cheb_order = 2,

@@ -1,6 +1,7 @@
 // Drop-in example: the reference call sequence (mesh -> space -> smoother -> Chebyshev ->
 // GMRES), written against include/semlab_b200.hpp instead of proj/core/include/semlab/*.hpp.
 // Built and run by tests/test_cpp_dropin_gpu.py; prints "OK <iterations> <rel_residual>".
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -29,6 +30,18 @@ int main() {
   check(semlab_space_build_rhs(space.handle(), 1, b.data()));
   GmresConfig cfg;
   GmresStats st = gmres_solve(A, &M, b, x, cfg);
+  // projection onto prior solutions (krylov.hpp:39-59): the guess for a solved b is its solution
+  ProjectionBasis proj(ctx, space.n(), 10);
+  proj.insert(x, A);
+  DeviceVector ug(space.n());
+  proj.initial_guess(b, ug);
+  const FieldVector xh = x.download(), uh = ug.download();
+  double du = 0.0, xn = 0.0;
+  for (size_t i = 0; i < xh.size(); ++i) {
+    du = std::max(du, std::abs(uh[i] - xh[i]));
+    xn = std::max(xn, std::abs(xh[i]));
+  }
+  if (proj.size() != 1 || !(du <= 1e-7 * xn)) { std::printf("FAIL projection %.3e\n", du / xn); return 1; }
   // exceptions mirror the reference: invalid parameters -> std::invalid_argument
   bool threw = false;
   try {
