@@ -69,6 +69,24 @@ def main():
     r = c.mask_inplace(np.random.default_rng(1).standard_normal(c.n))
     out["ras64"] = rel(gather(sch.apply(r[sl.local_slice()])), so.apply(r))
 
+    # Neumann mode over z-slabs: global mean removal (sem_space.cpp:207), unmasked diagonal,
+    # RAS with Neumann faces (schwarz.cpp:151-160; ASM is single-GPU only)
+    spn = S.SemSpace(mesh, p, S.NEUMANN)
+    cn = o.SemSpace(o.generate_kershaw(eps, E), p, o.NEUMANN)
+    out["ax_neumann"] = rel(gather(spn.apply_A(u[sl.local_slice()])), cn.apply_A(u))
+    out["diag_neumann"] = rel(gather(spn.stiffness_diag()), cn.stiffness_diag())
+    rn = np.random.default_rng(2).standard_normal(c.n)
+    out["ras64_neumann"] = rel(gather(S.SchwarzSmoother(spn, S.RAS, 64).apply(rn[sl.local_slice()])),
+                               o.SchwarzSmoother(cn, o.RAS, 64).apply(rn))
+    # ProjectionBasis (krylov.cpp:131-152) with rank-local owned-range reductions
+    X = np.random.default_rng(3).standard_normal((3, c.n))
+    pbg, pbo = S.ProjectionBasis(2), o.ProjectionBasis(2)
+    for x in X:
+        pbg.insert(sp.to_device(x[sl.local_slice()]), sp.as_linop())
+        pbo.insert(x, c.apply_A)
+    bb = np.random.default_rng(4).standard_normal(c.n)
+    out["proj"] = rel(gather(pbg.initial_guess(sp.to_device(bb[sl.local_slice()]))), pbo.initial_guess(bb))
+
     pm = S.Pmg(mesh, (7, 3, 1), S.RAS_SMOOTHER, 2, 0.1, 1.1, 64, S.COARSE_DIRECT)
     pmo = o.Pmg(o.generate_kershaw(eps, E), (7, 3, 1), "ras", 2, 0.1, 1.1, "direct", 64)
     out["lam"] = [abs(pm.lam(l) - pmo.levels[l]["lam"]) / pmo.levels[l]["lam"] for l in range(2)]

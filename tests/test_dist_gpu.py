@@ -31,6 +31,9 @@ def test_distributed_matches_oracle(nproc):
     assert r["dot"] < 1e-12
     assert r["mass"] < 1e-13 and r["diag"] < 1e-12
     assert r["ras64"] < 1e-12
+    assert r["ax_neumann"] < 1e-12 and r["diag_neumann"] < 1e-12, r
+    assert r["ras64_neumann"] < 1e-12, r
+    assert r["proj"] < 1e-11, r
     assert max(r["lam"]) < 1e-9
     assert r["rhs"] < 1e-13
     for k in ("prolong0", "prolong1", "restrict0", "restrict1"):
