@@ -31,14 +31,16 @@ bool dist_ras_enabled() {
   return on;
 }
 
+// The fused paths apply A through the Ax epilogues, which do not remove the mean: Neumann
+// spaces (sem_space.cpp:207) take the generic path (A->apply, then S->apply).
 bool fused_jacobi(semlab_op S, semlab_op A) {
   return S->kind == semlab_op_s::kJacobi && A->kind == semlab_op_s::kA && S->space == A->space &&
-         !A->space->distributed();
+         !A->space->distributed() && A->space->bc == SEMLAB_BC_DIRICHLET;
 }
 
 bool fused_ras(semlab_op S, semlab_op A) {
   return S->kind == semlab_op_s::kSchwarz && S->sch->mode == SEMLAB_SCHWARZ_RAS && A->kind == semlab_op_s::kA &&
-         S->space == A->space && !A->space->distributed();
+         S->space == A->space && !A->space->distributed() && A->space->bc == SEMLAB_BC_DIRICHLET;
 }
 
 bool dist_ras(semlab_op S, semlab_op A) {

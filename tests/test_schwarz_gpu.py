@@ -130,3 +130,27 @@ def test_schwarz_neumann_fp32(ctx, mode):
     z = S.SchwarzSmoother(g, mode, 32).apply(r)
     assert rel(z, o.SchwarzSmoother(c, mode, 64).apply(r)) < 2e-5
     assert rel(z, o.SchwarzSmoother(c, mode, 32).apply(r)) < 2e-6
+
+
+@pytest.mark.parametrize("smoother", ["ras", "jacobi"])
+@pytest.mark.parametrize("x0_zero", [True, False])
+def test_chebyshev_neumann_matches_oracle(ctx, smoother, x0_zero):
+    """Chebyshev smoothing of the Neumann operator (A with mean removal, sem_space.cpp:207): the
+    fused Ax/RAS epilogues skip the mean removal, so Neumann spaces take the generic path."""
+    from paper_2110_07663_b200 import semlab as S
+    g = S.SemSpace(S.generate_kershaw(0.3, 4, ctx), 5, S.NEUMANN)
+    c = o.SemSpace(o.generate_kershaw(0.3, 4), 5, o.NEUMANN)
+    if smoother == "ras":
+        Sg, So = S.SchwarzSmoother(g, S.RAS, 64).as_linop(), o.SchwarzSmoother(c, o.RAS, 64).apply
+    else:
+        inv = o.jacobi_inverse_diag(c)
+        Sg, So = g.jacobi(), (lambda v: inv * v)
+    cg = S.ChebyshevSmoother(Sg, g.as_linop(), S.ChebyParams(2, 0.1, 1.1, 3.0))
+    co = o.ChebyshevSmoother(So, c.apply_A, o.ChebyParams(2, 0.1, 1.1, 3.0))
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(c.n)
+    x = np.zeros(c.n) if x0_zero else rng.standard_normal(c.n)
+    xg = g.to_device(x)
+    cg.smooth(g.to_device(b), xg)
+    co.smooth(b, x)
+    assert rel(xg, x) < 1e-11
