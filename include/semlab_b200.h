@@ -34,6 +34,10 @@ extern "C" {
 const char* semlab_last_error(void);
 /* Library version string. */
 const char* semlab_version(void);
+/* Test/debug knob (no reference analogue): cap the grid of the persistent grid-stride kernels
+   (fused Ax, warp-per-element RAS) at max_ctas CTAs so every warp runs many elements even on a
+   small mesh; results must not change. 0 restores the occupancy-sized grid. Process-wide. */
+int semlab_debug_set_grid_cap(int max_ctas);
 
 /* ---- opaque handles ---------------------------------------------------------------------- */
 typedef struct semlab_ctx_s* semlab_ctx;         /* device + stream (+ NCCL communicator)  */
@@ -92,7 +96,8 @@ typedef struct { /* GmresStats, krylov.hpp:17-25 (history copied into a caller b
 } semlab_gmres_stats;
 
 /* ---- context ------------------------------------------------------------------------------ */
-/* One context per process and GPU. All work is ordered on cuda_stream (a cudaStream_t;
+/* One GPU per process: all contexts alive in a process must use the same device (a second
+   device is refused with SEMLAB_EINVAL). All work is ordered on cuda_stream (a cudaStream_t;
    NULL = the device's default stream, as in the CUDA runtime). */
 int semlab_ctx_create(int device, void* cuda_stream, semlab_ctx* out);
 /* Multi-GPU: rank/nranks over NCCL; nccl_id is the 128-byte ncclUniqueId from rank 0. */
@@ -130,6 +135,9 @@ int semlab_space_destroy(semlab_space s);
 int semlab_space_sizes(semlab_space s, int64_t out[11]);
 /* apply_A, sem_space.cpp:195-209: out = mask o Q^T A_L Q o mask (in). */
 int semlab_space_apply_A(semlab_space s, const double* d_in, double* d_out);
+/* Extension (no reference analogue): apply_A with the geometric factors rounded to FP32 and FP64
+   arithmetic, the operator of the FP32 smoother (order 7 only; EINVAL otherwise). */
+int semlab_space_apply_A_geom32(semlab_space s, const double* d_in, double* d_out);
 /* apply_local_stiffness on every element (E-vector in/out), sem_space.cpp:127-180. */
 int semlab_space_apply_local_stiffness(semlab_space s, const double* d_local_in, double* d_local_out);
 /* gather (Q^T) / scatter (Q) / gather_scatter (QQ^T), sem_space.cpp:110-125, hpp:86-88. */

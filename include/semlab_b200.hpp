@@ -31,6 +31,39 @@ inline void check(int rc) {
   throw std::runtime_error(msg);
 }
 
+// Move-only owner of a C handle: every wrapper object below owns exactly one handle, so a copy
+// (vector push_back, reallocation) can never destroy it twice. Moves transfer ownership.
+template <class H, int (*Destroy)(H)>
+class Owned {
+ public:
+  Owned() = default;
+  explicit Owned(H h) : h_(h) {}
+  Owned(Owned&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  Owned& operator=(Owned&& o) noexcept {
+    if (this != &o) {
+      reset();
+      h_ = o.h_;
+      o.h_ = nullptr;
+    }
+    return *this;
+  }
+  Owned(const Owned&) = delete;
+  Owned& operator=(const Owned&) = delete;
+  ~Owned() { reset(); }
+  void reset() {
+    if (h_) Destroy(h_);
+    h_ = nullptr;
+  }
+  H get() const { return h_; }
+  H* out() {
+    reset();
+    return &h_;
+  }
+
+ private:
+  H h_ = nullptr;
+};
+
 class DeviceVector {  // owning device buffer
  public:
   DeviceVector() = default;
@@ -40,7 +73,18 @@ class DeviceVector {  // owning device buffer
   }
   DeviceVector(const FieldVector& h) : DeviceVector(Index(h.size())) { upload(h); }
   DeviceVector(const DeviceVector&) = delete;
+  DeviceVector& operator=(const DeviceVector&) = delete;
   DeviceVector(DeviceVector&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DeviceVector& operator=(DeviceVector&& o) noexcept {
+    if (this != &o) {
+      if (p_) cudaFree(p_);
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
   ~DeviceVector() { if (p_) cudaFree(p_); }
   double* data() { return p_; }
   const double* data() const { return p_; }
@@ -59,14 +103,12 @@ class DeviceVector {  // owning device buffer
 
 class Context {
  public:
-  explicit Context(int device = 0, cudaStream_t stream = nullptr) { check(semlab_ctx_create(device, stream, &h_)); }
-  ~Context() { semlab_ctx_destroy(h_); }
-  Context(const Context&) = delete;
-  semlab_ctx handle() const { return h_; }
-  void synchronize() const { check(semlab_ctx_synchronize(h_)); }
+  explicit Context(int device = 0, cudaStream_t stream = nullptr) { check(semlab_ctx_create(device, stream, h_.out())); }
+  semlab_ctx handle() const { return h_.get(); }
+  void synchronize() const { check(semlab_ctx_synchronize(h_.get())); }
 
  private:
-  semlab_ctx h_ = nullptr;
+  Owned<semlab_ctx, semlab_ctx_destroy> h_;
 };
 
 struct KershawParams {  // mesh.hpp:17-20
@@ -81,49 +123,47 @@ class HexMesh {  // mesh.hpp:44-100
   static std::shared_ptr<HexMesh> box(Context& ctx, std::array<int, 3> dims, std::array<double, 3> lo,
                                       std::array<double, 3> hi) {
     auto m = std::shared_ptr<HexMesh>(new HexMesh);
-    check(semlab_mesh_box(ctx.handle(), dims.data(), lo.data(), hi.data(), &m->h_));
+    check(semlab_mesh_box(ctx.handle(), dims.data(), lo.data(), hi.data(), m->h_.out()));
     return m;
   }
-  ~HexMesh() { semlab_mesh_destroy(h_); }
-  semlab_mesh handle() const { return h_; }
+  semlab_mesh handle() const { return h_.get(); }
 
  private:
   HexMesh() = default;
   friend std::shared_ptr<HexMesh> generate_kershaw(Context&, const KershawParams&, int);
-  semlab_mesh h_ = nullptr;
+  Owned<semlab_mesh, semlab_mesh_destroy> h_;
 };
 
 // generate_kershaw(params, p), mesh.cpp:138-171 (p is accepted for signature parity)
 inline std::shared_ptr<HexMesh> generate_kershaw(Context& ctx, const KershawParams& params, int /*p*/) {
   auto m = std::shared_ptr<HexMesh>(new HexMesh);
-  check(semlab_mesh_kershaw(ctx.handle(), params.eps, params.elements_per_axis, &m->h_));
+  check(semlab_mesh_kershaw(ctx.handle(), params.eps, params.elements_per_axis, m->h_.out()));
   return m;
 }
 
 class LinOp {  // types.hpp:13 (device-resident operator)
+  // Copyable like the reference's std::function: copies share the one native operator, which is
+  // destroyed with the last copy. Objects that use a LinOp (ChebyshevSmoother) keep a copy.
  public:
-  explicit LinOp(semlab_op h = nullptr, bool own = true) : h_(h), own_(own) {}
-  LinOp(LinOp&& o) noexcept : h_(o.h_), own_(o.own_) { o.h_ = nullptr; }
-  LinOp(const LinOp&) = delete;
-  ~LinOp() { if (h_ && own_) semlab_op_destroy(h_); }
+  LinOp() = default;
+  explicit LinOp(semlab_op h) : h_(h, [](semlab_op o) { semlab_op_destroy(o); }) {}
   explicit operator bool() const { return h_ != nullptr; }
-  semlab_op handle() const { return h_; }
-  void operator()(const DeviceVector& in, DeviceVector& out) const { check(semlab_op_apply(h_, in.data(), out.data())); }
+  semlab_op handle() const { return h_.get(); }
+  void operator()(const DeviceVector& in, DeviceVector& out) const {
+    check(semlab_op_apply(h_.get(), in.data(), out.data()));
+  }
 
  private:
-  semlab_op h_;
-  bool own_;
+  std::shared_ptr<semlab_op_s> h_;
 };
 
 class SemSpace {  // sem_space.hpp:26-129
  public:
   SemSpace(std::shared_ptr<HexMesh> mesh, int order, BcMode bc = BcMode::Dirichlet) : mesh_(std::move(mesh)) {
-    check(semlab_space_create(mesh_->handle(), order, int(bc), &h_));
-    check(semlab_space_sizes(h_, sizes_));
+    check(semlab_space_create(mesh_->handle(), order, int(bc), h_.out()));
+    check(semlab_space_sizes(h_.get(), sizes_));
   }
-  ~SemSpace() { semlab_space_destroy(h_); }
-  SemSpace(const SemSpace&) = delete;
-  semlab_space handle() const { return h_; }
+  semlab_space handle() const { return h_.get(); }
   Index n() const { return sizes_[0]; }
   Index n_free() const { return sizes_[1]; }
   Index n_local_total() const { return sizes_[2]; }
@@ -133,63 +173,62 @@ class SemSpace {  // sem_space.hpp:26-129
     apply_A(du, dw);
     return dw.download();
   }
-  void apply_A(const DeviceVector& u, DeviceVector& w) const { check(semlab_space_apply_A(h_, u.data(), w.data())); }
+  void apply_A(const DeviceVector& u, DeviceVector& w) const { check(semlab_space_apply_A(h_.get(), u.data(), w.data())); }
   FieldVector stiffness_diag() const {
     DeviceVector d(n());
-    check(semlab_space_stiffness_diag(h_, d.data()));
+    check(semlab_space_stiffness_diag(h_.get(), d.data()));
     return d.download();
   }
   FieldVector mass_diag() const {
     DeviceVector d(n());
-    check(semlab_space_mass_diag(h_, d.data()));
+    check(semlab_space_mass_diag(h_.get(), d.data()));
     return d.download();
   }
   FieldVector gather(const FieldVector& local) const {
     DeviceVector dl(local), dg(n());
-    check(semlab_space_gather(h_, dl.data(), dg.data()));
+    check(semlab_space_gather(h_.get(), dl.data(), dg.data()));
     return dg.download();
   }
   FieldVector scatter(const FieldVector& global) const {
     DeviceVector dg(global), dl(n_local_total());
-    check(semlab_space_scatter(h_, dg.data(), dl.data()));
+    check(semlab_space_scatter(h_.get(), dg.data(), dl.data()));
     return dl.download();
   }
   LinOp as_linop() const {
     semlab_op o;
-    check(semlab_op_A(h_, &o));
+    check(semlab_op_A(h_.get(), &o));
     return LinOp(o);
   }
   LinOp jacobi() const {
     semlab_op o;
-    check(semlab_op_jacobi(h_, &o));
+    check(semlab_op_jacobi(h_.get(), &o));
     return LinOp(o);
   }
 
  private:
   std::shared_ptr<HexMesh> mesh_;
-  semlab_space h_ = nullptr;
+  Owned<semlab_space, semlab_space_destroy> h_;
   int64_t sizes_[11] = {};
 };
 
 class SchwarzSmoother {  // schwarz.hpp:31-86 (precision: 32 = paper's FP32 FDM, 64 = reference arithmetic)
  public:
   SchwarzSmoother(const SemSpace& space, SchwarzMode mode, int precision = 32) : n_(space.n()) {
-    check(semlab_schwarz_create(space.handle(), int(mode), precision, &h_));
+    check(semlab_schwarz_create(space.handle(), int(mode), precision, h_.out()));
   }
-  ~SchwarzSmoother() { semlab_schwarz_destroy(h_); }
   FieldVector apply(const FieldVector& r) const {
     DeviceVector dr(r), dz(n_);
-    check(semlab_schwarz_apply(h_, dr.data(), dz.data()));
+    check(semlab_schwarz_apply(h_.get(), dr.data(), dz.data()));
     return dz.download();
   }
   LinOp as_linop() const {
     semlab_op o;
-    check(semlab_op_schwarz(h_, &o));
+    check(semlab_op_schwarz(h_.get(), &o));
     return LinOp(o);
   }
 
  private:
-  semlab_schwarz h_ = nullptr;
+  Owned<semlab_schwarz, semlab_schwarz_destroy> h_;
   Index n_;
 };
 
@@ -213,16 +252,21 @@ inline LambdaEstimate estimate_lambda_max(const LinOp& S, const LinOp& A, Index 
 }
 
 class ChebyshevSmoother {  // chebyshev.hpp:36-46
+  // Takes its operators by value like the reference (chebyshev.hpp:36) and keeps them: the C
+  // object only borrows the native operators, so temporaries such as
+  // ChebyshevSmoother c(sch.as_linop(), sp.as_linop(), p) stay alive as long as the smoother.
  public:
-  ChebyshevSmoother(const LinOp& S, const LinOp& A, const ChebyParams& p) {
+  ChebyshevSmoother(LinOp S, LinOp A, const ChebyParams& p) : S_(std::move(S)), A_(std::move(A)) {
     semlab_cheby_params cp{p.order, p.lambda_min_mult, p.lambda_max_mult, p.lambda_max_est};
-    check(semlab_cheby_create(S.handle(), A.handle(), &cp, &h_));
+    check(semlab_cheby_create(S_.handle(), A_.handle(), &cp, h_.out()));
   }
-  ~ChebyshevSmoother() { semlab_cheby_destroy(h_); }
-  void smooth(const DeviceVector& b, DeviceVector& x) const { check(semlab_cheby_smooth(h_, b.data(), x.data())); }
+  void smooth(const DeviceVector& b, DeviceVector& x) const {
+    check(semlab_cheby_smooth(h_.get(), b.data(), x.data()));
+  }
 
  private:
-  semlab_cheby h_ = nullptr;
+  LinOp S_, A_;  // declared before h_: destroyed after the smoother that borrows them
+  Owned<semlab_cheby, semlab_cheby_destroy> h_;
 };
 
 // ProjectionBasis, krylov.hpp:39-59. The device basis needs its context and vector length up
@@ -230,27 +274,25 @@ class ChebyshevSmoother {  // chebyshev.hpp:36-46
 class ProjectionBasis {
  public:
   ProjectionBasis(const Context& ctx, Index n, int capacity = 10) : capacity_(capacity) {
-    check(semlab_proj_create(ctx.handle(), n, capacity, &h_));
+    check(semlab_proj_create(ctx.handle(), n, capacity, h_.out()));
   }
-  ~ProjectionBasis() { semlab_proj_destroy(h_); }
-  ProjectionBasis(const ProjectionBasis&) = delete;
   void initial_guess(const DeviceVector& b, DeviceVector& u) const {
-    check(semlab_proj_initial_guess(h_, b.data(), u.data()));
+    check(semlab_proj_initial_guess(h_.get(), b.data(), u.data()));
   }
   void insert(const DeviceVector& x, const LinOp& A) {
     if (!A) throw std::invalid_argument("ProjectionBasis: missing operator");
-    check(semlab_proj_insert(h_, x.data(), A.handle()));
+    check(semlab_proj_insert(h_.get(), x.data(), A.handle()));
   }
   int size() const {
     int k = 0;
-    check(semlab_proj_size(h_, &k));
+    check(semlab_proj_size(h_.get(), &k));
     return k;
   }
   int capacity() const { return capacity_; }
-  void clear() { check(semlab_proj_clear(h_)); }
+  void clear() { check(semlab_proj_clear(h_.get())); }
 
  private:
-  semlab_proj h_ = nullptr;
+  Owned<semlab_proj, semlab_proj_destroy> h_;
   int capacity_;
 };
 
@@ -260,23 +302,22 @@ class Pmg {  // pMG V-cycle (pmg.cpp missing in the reference)
       int precision = 32, int coarse = SEMLAB_COARSE_AMG)
       : mesh_(std::move(mesh)) {
     check(semlab_pmg_create(mesh_->handle(), int(orders.size()), orders.data(), smoother, cheb_order, 0.1, 1.1,
-                            precision, coarse, &h_));
+                            precision, coarse, h_.out()));
   }
-  ~Pmg() { semlab_pmg_destroy(h_); }
   semlab_space fine_space() const {
     semlab_space s;
-    check(semlab_pmg_space(h_, 0, &s));
+    check(semlab_pmg_space(h_.get(), 0, &s));
     return s;
   }
   LinOp as_linop() const {
     semlab_op o;
-    check(semlab_op_pmg(h_, &o));
+    check(semlab_op_pmg(h_.get(), &o));
     return LinOp(o);
   }
 
  private:
   std::shared_ptr<HexMesh> mesh_;
-  semlab_pmg h_ = nullptr;
+  Owned<semlab_pmg, semlab_pmg_destroy> h_;
 };
 
 struct GmresConfig {  // krylov.hpp:9-15

@@ -270,4 +270,120 @@ int ref_solve(double eps, int E, const int* orders, int nlev, const char* precon
   });
 }
 
+// ---- handle-based cases (tests/golden/make_golden_scale.py): the mesh, spaces, smoothers and pMG of
+// one configuration are built once and reused for every output at BASELINE sizes (E = 8^3 .. 32^3).
+struct RefCase {
+  HexMesh mesh;
+  std::unique_ptr<Pmg> pmg;
+  std::unique_ptr<SemSpace> own;
+  const SemSpace* s0 = nullptr;
+  FieldVector inv;
+  LinOp A, M;
+  std::unique_ptr<SchwarzSmoother> ras, asm_;
+  RefCase(double eps, int E, int p) : mesh(mesh_of(eps, E, p)) {}
+};
+
+void* ref_case_create(double eps, int E, const int* orders, int nlev, const char* precond, const char* coarse,
+                      int eta) {
+  RefCase* c = nullptr;
+  const int rc = guard([&] {
+    auto cs = std::make_unique<RefCase>(eps, E, orders[0]);
+    const std::string pc(precond);
+    if (pc == "none" || (pc == "jacobi" && nlev == 1)) {
+      cs->own = std::make_unique<SemSpace>(cs->mesh, orders[0]);
+      cs->s0 = cs->own.get();
+      if (pc == "jacobi") {
+        cs->inv = jacobi_inverse_diag(*cs->s0);
+        const FieldVector* inv = &cs->inv;
+        cs->M = [inv](const FieldVector& in, FieldVector& out) { out = inv->cwiseProduct(in); };
+      }
+    } else {
+      cs->pmg = std::make_unique<Pmg>(cs->mesh, orders_of(orders, nlev), pc, eta, 0.1, 1.1, coarse);
+      cs->s0 = cs->pmg->spaces[0].get();
+      cs->M = cs->pmg->as_linop();
+    }
+    const SemSpace* s0 = cs->s0;
+    cs->A = [s0](const FieldVector& in, FieldVector& out) { out = s0->apply_A(in); };
+    c = cs.release();
+  });
+  return rc == 0 ? c : nullptr;
+}
+
+void ref_case_destroy(void* h) { delete static_cast<RefCase*>(h); }
+
+int64_t ref_case_n(void* h) { return static_cast<RefCase*>(h)->s0->n(); }
+
+int ref_case_apply_A(void* h, const double* u, double* out) {
+  return guard([&] {
+    auto* c = static_cast<RefCase*>(h);
+    FieldVector v = Eigen::Map<const Eigen::MatrixXd>(u, c->s0->n(), 1);
+    FieldVector w = c->s0->apply_A(v);
+    std::memcpy(out, w.data(), sizeof(double) * size_t(c->s0->n()));
+  });
+}
+
+int ref_case_diag(void* h, double* out) {
+  return guard([&] {
+    auto* c = static_cast<RefCase*>(h);
+    FieldVector d = c->s0->stiffness_diag();
+    std::memcpy(out, d.data(), sizeof(double) * size_t(c->s0->n()));
+  });
+}
+
+// mode 1 = RAS, 0 = ASM on the finest space (schwarz.cpp:242-289)
+int ref_case_schwarz(void* h, int mode, const double* r, double* z) {
+  return guard([&] {
+    auto* c = static_cast<RefCase*>(h);
+    auto& sch = mode == 1 ? c->ras : c->asm_;
+    if (!sch) sch = std::make_unique<SchwarzSmoother>(*c->s0, mode == 1 ? SchwarzMode::Ras : SchwarzMode::Asm);
+    FieldVector rv = Eigen::Map<const Eigen::MatrixXd>(r, c->s0->n(), 1);
+    FieldVector zv = sch->apply(rv);
+    std::memcpy(z, zv.data(), sizeof(double) * size_t(c->s0->n()));
+  });
+}
+
+int ref_case_rhs(void* h, uint64_t seed, double* out) {
+  return guard([&] {
+    auto* c = static_cast<RefCase*>(h);
+    FieldVector b = build_rhs(*c->s0, seed);
+    std::memcpy(out, b.data(), sizeof(double) * size_t(c->s0->n()));
+  });
+}
+
+// one V-cycle z = M b (pMG cases only); lams = the per-level lambda estimates
+int ref_case_vcycle(void* h, const double* b, double* z, double* lams) {
+  return guard([&] {
+    auto* c = static_cast<RefCase*>(h);
+    if (!c->pmg) throw std::invalid_argument("ref_case_vcycle: not a pMG case");
+    FieldVector bv = Eigen::Map<const Eigen::MatrixXd>(b, c->s0->n(), 1);
+    FieldVector zv = c->pmg->vcycle(bv);
+    std::memcpy(z, zv.data(), sizeof(double) * size_t(c->s0->n()));
+    for (size_t l = 0; l < c->pmg->levels.size(); ++l) lams[l] = c->pmg->levels[l].lam;
+  });
+}
+
+// full solve from x0 = 0 with b = build_rhs(seed 1): krylov 0 = GMRES(restart), 1 = PCG
+int ref_case_solve(void* h, int krylov, int restart, double tol, int max_iters, double* x, int* iters, double* rel_res,
+                   double* history, int hcap) {
+  return guard([&] {
+    auto* c = static_cast<RefCase*>(h);
+    FieldVector b = build_rhs(*c->s0, 1);
+    FieldVector xv = FieldVector::Zero(c->s0->n());
+    GmresStats st;
+    if (krylov == 0) {
+      GmresConfig cfg;
+      cfg.restart = restart;
+      cfg.tol = tol;
+      cfg.max_iters = max_iters;
+      st = gmres_solve(c->A, c->M, b, xv, cfg);
+    } else {
+      st = pcg_solve(c->A, c->M, b, xv, tol, max_iters);
+    }
+    std::memcpy(x, xv.data(), sizeof(double) * size_t(c->s0->n()));
+    *iters = st.iterations;
+    *rel_res = st.rel_residual;
+    for (int i = 0; i < hcap && i < int(st.history.size()); ++i) history[i] = st.history[size_t(i)];
+  });
+}
+
 }  // extern "C"

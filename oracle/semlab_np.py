@@ -351,6 +351,16 @@ class SemSpace:
         out = _d_r(DT, vr) + _d_s(DT, vs) + _d_t(DT, vt)
         return out.reshape(-1)
 
+    def with_geom32(self):
+        """A view of this space whose geometric factors are rounded to FP32 (arithmetic stays
+        FP64): the operator the B200 product's FP32 smoother applies at order 7 (its pMG levels'
+        smoother A, lambda estimate and V-cycle residual). Not a reference function: the reference
+        has no FP32 smoother; this pins that product variant to FP64-arithmetic ground truth."""
+        import copy
+        c = copy.copy(self)
+        c.geom = self.geom.astype(np.float32).astype(np.float64)
+        return c
+
     def apply_A(self, u):
         """mask o Q^T A_L Q o mask (Neumann: minus the mean) — sem_space.cpp:195-209."""
         v = self.mask_inplace(np.array(u, dtype=np.float64))
@@ -1118,7 +1128,9 @@ class Pmg:
         self.spaces = [SemSpace(mesh, q) for q in orders]
         self.levels = []
         for sp_ in self.spaces[:-1]:
-            A = sp_.apply_A
+            # precision 32 at order 7: the smoother's operator uses FP32-rounded factors, like the
+            # product (pmg.cpp build(): L.A->geom32); the Krylov operator is not part of Pmg
+            A = sp_.with_geom32().apply_A if (precision == 32 and sp_.order == 7) else sp_.apply_A
             if smoother == "jacobi":
                 inv = jacobi_inverse_diag(sp_)
                 S = (lambda inv: (lambda v: inv * v))(inv)

@@ -55,6 +55,7 @@ APPLY_FN = C.CFUNCTYPE(None, p, p, p)
 SIGNATURES = {
     "semlab_last_error": (C.c_char_p, []),
     "semlab_version": (C.c_char_p, []),
+    "semlab_debug_set_grid_cap": (i32, [i32]),
     "semlab_ctx_create": (i32, [i32, p, C.POINTER(p)]),
     "semlab_ctx_create_dist": (i32, [i32, p, i32, i32, p, C.POINTER(p)]),
     "semlab_nccl_get_unique_id": (i32, [p]),
@@ -70,6 +71,7 @@ SIGNATURES = {
     "semlab_space_destroy": (i32, [p]),
     "semlab_space_sizes": (i32, [p, pi64]),
     "semlab_space_apply_A": (i32, [p, p, p]),
+    "semlab_space_apply_A_geom32": (i32, [p, p, p]),
     "semlab_space_apply_local_stiffness": (i32, [p, p, p]),
     "semlab_space_gather": (i32, [p, p, p]),
     "semlab_space_scatter": (i32, [p, p, p]),

@@ -2,8 +2,11 @@
 // No exception crosses it: sb::Error / std::exception become status codes + semlab_last_error().
 #include <nccl.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 
 #include "capi_util.hpp"
@@ -17,6 +20,30 @@ thread_local std::string g_err;
 }
 
 void sb_set_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+std::atomic<int> g_grid_cap{0};
+std::mutex g_dev_mu;
+int g_ctx_device = -1;  // the one device this process's contexts use
+int g_ctx_live = 0;
+}  // namespace
+
+namespace sb {
+int grid_cap() { return g_grid_cap.load(std::memory_order_relaxed); }
+
+int per_device_once(const void* key, const std::function<int()>& init) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> cache;
+  int dev = 0;
+  SB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, key});
+  if (it != cache.end()) return it->second;
+  const int v = init();
+  cache[{dev, key}] = v;
+  return v;
+}
+}  // namespace sb
 
 int sb_guard_impl(const std::function<void()>& f) {
   try {
@@ -37,13 +64,34 @@ int sb_guard_impl(const std::function<void()>& f) {
 extern "C" {
 
 const char* semlab_last_error(void) { return g_err.c_str(); }
-const char* semlab_version(void) { return "semlab_b200 0.1 (sm_100a)"; }
+const char* semlab_version(void) { return "semlab_b200 0.2 (sm_100a)"; }
+
+int semlab_debug_set_grid_cap(int max_ctas) {
+  return guard([&] {
+    if (max_ctas < 0) invalid("semlab_debug_set_grid_cap: max_ctas must be >= 0");
+    g_grid_cap.store(max_ctas);
+  });
+}
 
 // ---------------------------------------------------------------- context
+static void register_ctx(int device) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  g_ctx_device = device;
+  ++g_ctx_live;
+}
+
 static void ctx_init(semlab_ctx c, int device, void* stream) {
   int ndev = 0;
   SB_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) invalid("semlab_ctx_create: no CUDA device " + std::to_string(device));
+  {
+    // One GPU per process (one rank per GPU): entry points run on the calling thread's current
+    // device, which the context sets here. A second device in the same process is refused.
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_ctx_live > 0 && g_ctx_device != device)
+      invalid("semlab_ctx_create: contexts of one process must share a device (live contexts use device " +
+              std::to_string(g_ctx_device) + ")");
+  }
   SB_CUDA(cudaSetDevice(device));
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);  // NULL = default stream (shared with the caller)
@@ -60,6 +108,7 @@ int semlab_ctx_create(int device, void* stream, semlab_ctx* out) {
     need(out, "semlab_ctx_create: out");
     auto c = std::make_unique<semlab_ctx_s>();
     ctx_init(c.get(), device, stream);
+    register_ctx(device);
     *out = c.release();
   });
 }
@@ -91,6 +140,7 @@ int semlab_ctx_create_dist(int device, void* stream, int rank, int nranks, const
       if (r != ncclSuccess) fail(kNccl, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
       c->nccl = comm;
     }
+    register_ctx(device);
     *out = c.release();
   });
 }
@@ -103,6 +153,8 @@ int semlab_ctx_destroy(semlab_ctx c) {
     if (c->host_pinned) cudaFreeHost(c->host_pinned);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_ctx_live > 0) --g_ctx_live;
   });
 }
 
@@ -229,6 +281,14 @@ int semlab_space_apply_A(semlab_space s, const double* in, double* out) {
   return guard([&] {
     need(s, "apply_A: space");
     s->apply_A(in, out);
+  });
+}
+
+int semlab_space_apply_A_geom32(semlab_space s, const double* in, double* out) {
+  return guard([&] {
+    need(s, "apply_A_geom32: space");
+    if (!s->enable_geom32()) invalid("apply_A_geom32: FP32 geometric factors exist for order 7 only");
+    s->apply_A(in, out, true);
   });
 }
 

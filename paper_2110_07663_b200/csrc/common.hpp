@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -35,6 +36,42 @@ struct Error : std::runtime_error {
 // Check the last launch (launch-configuration errors surface immediately; asynchronous
 // faults surface at the next synchronising call).
 #define SB_LAUNCH_CHECK() SB_CUDA(cudaGetLastError())
+
+// One-time launch configuration (cudaFuncSetAttribute, occupancy-derived grid sizes) cached per
+// (device, kernel): function attributes belong to a device's context, so a value computed on one
+// GPU is never reused on another.
+int per_device_once(const void* key, const std::function<int()>& init);
+
+// Test/debug cap on the grid of the grid-stride (persistent) kernels: with a cap of 1-2 CTAs every
+// warp runs many elements, which forces the multi-element paths of k_axw / k_rasw at small E.
+// 0 = no cap (the default). Set through semlab_debug_set_grid_cap().
+int grid_cap();
+// Resident CTAs of a kernel over the whole device (occupancy x SMs), with its dynamic shared memory
+// attribute set; cached per (device, kernel).
+template <class K>
+int resident_ctas(K kern, int threads, size_t smem) {
+  return per_device_once(reinterpret_cast<const void*>(kern), [&] {
+    if (smem > 48 * 1024)
+      SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0, dev = 0, sms = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    SB_CUDA(cudaGetDevice(&dev));
+    SB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return per_sm > 0 ? per_sm * sms : sms;
+  });
+}
+// Sets a kernel's dynamic shared memory attribute once per device.
+template <class K>
+void smem_attr(K kern, size_t smem) {
+  per_device_once(reinterpret_cast<const char*>(kern) + 1, [&] {  // key distinct from resident_ctas'
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    return 1;
+  });
+}
+inline int capped_grid(int64_t grid) {
+  const int c = grid_cap();
+  return int(c > 0 && grid > c ? c : grid);
+}
 
 // Geometry of this rank's z-slab of the structured element grid, passed by value to kernels.
 // Elements: e = ex + Ex (ey + Ey ez) globally (mesh.hpp:58-60); this rank owns element layers

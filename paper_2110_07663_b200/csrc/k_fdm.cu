@@ -793,11 +793,7 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_fdm_boxes(const
 
 template <class K>
 void prep(K kern, size_t smem) {
-  static std::mutex mu;
-  static std::unordered_set<const void*> done;
-  std::lock_guard<std::mutex> lk(mu);
-  if (done.insert(reinterpret_cast<const void*>(kern)).second)
-    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  smem_attr(kern, smem);
 }
 
 bool ras_warp() {
@@ -815,17 +811,9 @@ struct Launch {
   static void rasw(const Slab& sl, const T* S, const T* L, const double* r, const RasEpi& e, cudaStream_t s) {
     using W = WShape<P, T>;
     auto kern = k_rasw<P, T, MODE>;
-    prep(kern, W::smem());
-    static int per_sm = 0;
-    if (!per_sm) {
-      SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::NT, W::smem()));
-      int dev = 0, sms = 0;
-      SB_CUDA(cudaGetDevice(&dev));
-      SB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      per_sm = std::max(1, per_sm) * sms;
-    }
+    const int nctas = resident_ctas(kern, W::NT, W::smem());
     const int64_t need = (sl.elems() + W::WPC - 1) / W::WPC;
-    kern<<<int(std::min<int64_t>(need, per_sm)), W::NT, W::smem(), s>>>(sl, S, L, r, e);
+    kern<<<capped_grid(std::min<int64_t>(need, nctas)), W::NT, W::smem(), s>>>(sl, S, L, r, e);
   }
   template <int P>
   static void ras(const Slab& sl, const T* S, const T* L, const double* r, int mode, const RasEpi& e, cudaStream_t s) {

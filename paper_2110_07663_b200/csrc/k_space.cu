@@ -689,16 +689,8 @@ int64_t axp_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
     invalid("SemSpace: a rank's lattice must have < 2^31 nodes");
   const size_t smem = size_t(align128(geom_bytes<GT>(NLOC))) + (size_t(2) * NLOC + ND * ND) * sizeof(double);
   auto kern = k_axp<ND, EpiT, GT>;
-  static int nctas = 0;  // resident CTAs: occupancy x SMs (per instantiation)
-  if (nctas == 0) {
-    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0, dev = 0, sms = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ND * ND, smem));
-    SB_CUDA(cudaGetDevice(&dev));
-    SB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    nctas = std::max(1, per_sm * sms);
-  }
-  const int grid = int(std::min<int64_t>(nctas, nE));
+  const int nctas = resident_ctas(kern, ND * ND, smem);
+  const int grid = capped_grid(std::min<int64_t>(nctas, nE));
   kern<<<grid, ND * ND, smem, s>>>(sl, dmat<ND>(sl.q), u, geom, sy.dep, sy.flags, sy.ticket, int(nE + grid), epi);
   SB_LAUNCH_CHECK();
   return 1;
@@ -720,9 +712,6 @@ int64_t axp_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
 #ifndef SEMLAB_AXW_TMA
 #define SEMLAB_AXW_TMA 0  // whole-element geometry by one TMA bulk copy into shared memory, one element ahead
 #endif
-#ifndef SEMLAB_AXW_EXP
-#define SEMLAB_AXW_EXP 0  // timing experiments (wrong results): 1 no Q^T finish, 2 no DMMA
-#endif
 namespace axw {
 constexpr int PS = 72;  // z-layer stride (doubles): 64 + 8 so consecutive layers use opposite bank halves
 constexpr int ARR = 8 * PS;
@@ -730,11 +719,6 @@ __device__ __forceinline__ int sidx(int k, int j, int i) {  // swizzled workspac
   return k * PS + j * 8 + 2 * ((i >> 1) ^ ((j >> 1) & 3)) + (i & 1);
 }
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  if (SEMLAB_AXW_EXP == 2) {  // timing experiment only: no tensor-core work
-    c0 += a;
-    c1 += b;
-    return;
-  }
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
@@ -1092,7 +1076,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
     }
     // the release of this element is deferred until the next element's u has been gathered
     // (its MEMBAR then finds the deposits long acknowledged instead of stalling the warp)
-    if (prev >= 0 && SEMLAB_AXW_EXP != 1) finish_prev(prev);
+    if (prev >= 0) finish_prev(prev);
 #if !SEMLAB_AXW_PDEP
 #pragma unroll
     for (int t = 0; t < 16; ++t) pprev[t] = o[t];
@@ -1104,7 +1088,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
   }
   __syncwarp();
   if (lane == 0) st_release(&flags[prev], target);
-  if (SEMLAB_AXW_EXP != 1) finish_prev(prev);
+  finish_prev(prev);
 }
 
 template <class EpiT, class GT>
@@ -1118,16 +1102,8 @@ int64_t axw_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
   constexpr int W = SEMLAB_AXW_WARPS;
   const size_t smem = size_t(W) * axw_warp_doubles<GT>() * sizeof(double) + size_t(W) * 8;
   auto kern = k_axw<EpiT, GT>;
-  static int nctas = 0;
-  if (nctas == 0) {
-    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0, dev = 0, sms = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem));
-    SB_CUDA(cudaGetDevice(&dev));
-    SB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    nctas = std::max(1, per_sm * sms);
-  }
-  const int grid = int(std::min<int64_t>(nctas, (nE + W - 1) / W));
+  const int nctas = resident_ctas(kern, 32 * W, smem);
+  const int grid = capped_grid(std::min<int64_t>(nctas, (nE + W - 1) / W));
   kern<<<grid, 32 * W, smem, s>>>(sl, dmat<8>(sl.q), u, geom, sy.dep, sy.flags, sy.ticket, int(nE + int64_t(grid) * W),
                                    epi);
   SB_LAUNCH_CHECK();
@@ -1211,11 +1187,7 @@ int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, cons
   // epilogue (two fully parallel launches instead of CTAs idling on neighbour counters)
   constexpr int IO = LOCAL ? 1 : (ND <= SEMLAB_AX_SPLIT_ND ? 2 : 0);
   auto kern = k_ax<ND, EPB, IO, EpiT>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = true;
-  }
+  smem_attr(kern, smem);
   kern<<<ngroups, EPB * ND * ND, smem, s>>>(sl, dmat<ND>(sl.q), u, geom, sy.dep, sy.flags, sy.ticket, ngroups,
                                            IO == 2 ? sy.dep : out_local, epi);
   SB_LAUNCH_CHECK();

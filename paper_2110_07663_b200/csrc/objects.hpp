@@ -55,6 +55,7 @@ struct semlab_space_s {
   int64_t n = 0, E = 0, nloc = 0;
   std::vector<double> coords;  // host lattice coords of the local planes (3 per point)
   sb::DevBuf<double> geom, massw, mass_diag, inv_diag, dep, scratch_e, plane_lo, plane_hi;
+  sb::DevBuf<double> ones;  // Neumann mean removal (sem_space.cpp:207): the all-ones vector
   sb::DevBuf<unsigned> flags, ticket;
   sb::DevBuf<float> geom32;  // FP32-rounded geometric factors (the smoother's operator, order 7)
   bool has_inv_diag = false;

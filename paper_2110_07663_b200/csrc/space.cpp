@@ -125,17 +125,9 @@ void semlab_space_s::build() {
 // Interface planes z = ez0 q (shared with rank-1) and z = ez1 q (shared with rank+1) hold this
 // rank's partial Q^T sums after a gather-type operation; both ranks add lower + upper partial in
 // that order, so the duplicated planes stay bitwise identical on the two ranks.
-// SEMLAB_NO_EXCHANGE=1 turns the slab exchanges into no-ops: timing experiments only (wrong results).
-static bool no_exchange() {
-  static const bool on = [] {
-    const char* e = std::getenv("SEMLAB_NO_EXCHANGE");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
 
 void semlab_space_s::interface_sum(double* v) {
-  if (!distributed() || no_exchange()) return;
+  if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
   if (plane_lo.n < size_t(P)) {
     plane_lo.alloc(size_t(P));
@@ -164,7 +156,7 @@ void semlab_space_s::interface_sum(double* v) {
 // operator the planes next to the interface are already final on their owner, so the partial
 // interface planes and the Schwarz ghost planes travel together (one latency instead of two).
 void semlab_space_s::interface_sum_halo(double* v) {
-  if (!distributed() || no_exchange()) return;
+  if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
   if (plane_lo.n < size_t(P)) {
     plane_lo.alloc(size_t(P));
@@ -196,7 +188,7 @@ void semlab_space_s::interface_sum_halo(double* v) {
 
 // owner_copy_up of up to three vectors in one grouped call.
 void semlab_space_s::owner_copy_up_n(double* const* vs, int k) {
-  if (!distributed() || no_exchange()) return;
+  if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
   cudaStream_t s = ctx->stream;
@@ -214,7 +206,7 @@ void semlab_space_s::owner_copy_up_n(double* const* vs, int k) {
 
 // Ghost planes z = ez0 q - 1 and z = ez1 q + 1 (the Schwarz halo, schwarz.cpp:159-168).
 void semlab_space_s::halo_exchange(double* v) {
-  if (!distributed() || no_exchange()) return;
+  if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
   cudaStream_t s = ctx->stream;
@@ -235,7 +227,7 @@ void semlab_space_s::halo_exchange(double* v) {
 // The interface plane z = ez1 q is owned by the lower rank for owner-write operators (RAS):
 // copy it up so both ranks hold the owner's value.
 void semlab_space_s::owner_copy_up(double* v) {
-  if (!distributed() || no_exchange()) return;
+  if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
   cudaStream_t s = ctx->stream;
@@ -269,7 +261,6 @@ void semlab_space_s::apply_A(const double* in, double* out, bool g32) {
   ax(in, Epi::Write, a, g32);
   interface_sum(out);
   if (bc == SEMLAB_BC_NEUMANN) {  // r -= mean(r) (sem_space.cpp:207)
-    static thread_local DevBuf<double> ones;
     if (ones.n < size_t(n)) {
       ones.alloc(size_t(n));
       ctx->count(launch_fill(ones.p, n, 1.0, ctx->stream));

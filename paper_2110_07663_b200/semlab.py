@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -32,8 +33,11 @@ def _ptr(t: torch.Tensor) -> int:
 def _own(obj, handle, destroy, *parents):
     """Record obj's native handle in a box its parents also list. A cycle of garbage is finalised
     in arbitrary order, so releasing a parent first releases every child box still live: handles
-    are always destroyed child-before-parent (objects.hpp: smoother -> space -> mesh -> context)."""
-    box = [handle, destroy, []]
+    are always destroyed child-before-parent (objects.hpp: smoother -> space -> mesh -> context).
+    The box also holds a weak reference to obj: when a parent's release destroys the handle, obj's
+    .handle is cleared, so a later call raises (NULL handle -> ValueError) instead of touching
+    freed device memory."""
+    box = [handle, destroy, [], weakref.ref(obj)]
     obj._box = box
     for par in parents:
         pb = getattr(par, "_box", None)
@@ -57,6 +61,9 @@ def _release_box(box):
             _release_box(child)
         h, box[0] = box[0], None
         box[1](h)
+        obj = box[3]() if len(box) > 3 else None
+        if obj is not None:
+            obj.handle = None
 
 
 class Context:
@@ -232,6 +239,13 @@ class SemSpace:
         check(lib.semlab_space_apply_A(self.handle, _ptr(u), _ptr(out)))
         return out
 
+    def apply_A_geom32(self, u, out: torch.Tensor | None = None) -> torch.Tensor:
+        """apply_A with FP32-rounded geometric factors (the FP32 smoother's operator, order 7)."""
+        u = self.to_device(u)
+        out = self.zeros() if out is None else out
+        check(lib.semlab_space_apply_A_geom32(self.handle, _ptr(u), _ptr(out)))
+        return out
+
     def apply_local_stiffness(self, local) -> torch.Tensor:
         local = self.to_device(local)
         out = self.zeros(self.n_local_total)
@@ -397,8 +411,7 @@ class Pmg:
         for lvl in range(len(orders)):
             sh = C.c_void_p()
             check(lib.semlab_pmg_space(h, lvl, C.byref(sh)))
-            self.spaces.append(_BorrowedSpace(sh, mesh, orders[lvl]))
-            self.spaces[-1]._box = self._box  # smoothers built on a level are children of the hierarchy
+            self.spaces.append(_BorrowedSpace(sh, mesh, orders[lvl], self))
         self.n = self.spaces[0].n
 
     def lam(self, level: int) -> float:
@@ -431,12 +444,15 @@ class Pmg:
 
 
 class _BorrowedSpace(SemSpace):
-    """A SemSpace owned by a Pmg hierarchy (not destroyed from Python)."""
+    """A SemSpace owned by a Pmg hierarchy (destroyed with it, never from Python). It keeps its
+    Pmg alive (self._owner), and objects built on it (smoothers, operators) register as children
+    of the Pmg's box, so they are released before the hierarchy frees the space."""
 
-    def __init__(self, handle, mesh, order):
+    def __init__(self, handle, mesh, order, owner):
         self.mesh, self.order, self.bc, self.ctx = mesh, order, DIRICHLET, mesh.ctx
+        self._owner = owner
+        self._box = owner._box
         self.handle = None
-        self._h = handle
         s = (C.c_int64 * 11)()
         check(lib.semlab_space_sizes(handle, s))
         (self.n, self.n_free, self.n_local_total, nx, ny, nz, self.n_global, self.n_elements,
@@ -544,6 +560,11 @@ class ProjectionBasis:
 
     def __del__(self):
         _release(self)
+
+
+def debug_set_grid_cap(max_ctas: int) -> None:
+    """Cap the persistent kernels' grids (0 = occupancy-sized): forces many elements per warp."""
+    check(lib.semlab_debug_set_grid_cap(int(max_ctas)))
 
 
 def host_gll(order: int):

@@ -4,8 +4,16 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <type_traits>
+#include <vector>
 
 #include "semlab_b200.hpp"
+
+// handle-owning wrappers are move-only (a copy would destroy the native handle twice)
+static_assert(!std::is_copy_constructible<semlab_b200::SchwarzSmoother>::value, "copyable smoother");
+static_assert(std::is_move_constructible<semlab_b200::SchwarzSmoother>::value, "immovable smoother");
+static_assert(!std::is_copy_constructible<semlab_b200::Pmg>::value, "copyable pmg");
+static_assert(std::is_copy_constructible<semlab_b200::LinOp>::value, "LinOp is copyable like std::function");
 
 int main() {
   using namespace semlab_b200;
@@ -23,6 +31,21 @@ int main() {
   LinOp A = space.as_linop(), S = ras.as_linop();
   const LambdaEstimate lam = estimate_lambda_max(S, A, space.n(), 10, 0);
   ChebyshevSmoother cheb(S, A, ChebyParams{2, 0.1, 1.1, lam.value});
+  // the reference's temporary-operator form: the smoother keeps its LinOps alive
+  ChebyshevSmoother cheb_tmp(ras.as_linop(), space.as_linop(), ChebyParams{2, 0.1, 1.1, lam.value});
+  {
+    DeviceVector bb(space.n()), x1(space.n()), x2(space.n());
+    check(semlab_space_build_rhs(space.handle(), 1, bb.data()));
+    cheb.smooth(bb, x1);
+    cheb_tmp.smooth(bb, x2);
+    const FieldVector h1 = x1.download(), h2 = x2.download();
+    if (h1 != h2) { std::printf("FAIL temporary-LinOp smoother\n"); return 1; }
+  }
+  // wrappers move through containers without double destruction
+  std::vector<SchwarzSmoother> smoothers;
+  smoothers.emplace_back(space, SchwarzMode::Ras, 32);
+  smoothers.emplace_back(space, SchwarzMode::Asm, 64);
+  smoothers.emplace_back(space, SchwarzMode::Ras, 64);
   // pMG-preconditioned GMRES(20) to 1e-8 (krylov.hpp)
   Pmg pmg(mesh, {7, 3, 1}, SEMLAB_SMOOTHER_RAS, 2, 32, SEMLAB_COARSE_DIRECT);
   LinOp M = pmg.as_linop();
