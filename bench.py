@@ -90,60 +90,125 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------- CPU baselines
-def cpu_reference_sample(cfg, seconds=15.0):
-    """The reference's CPU path on host cores: oracle/_ref (the reference's own sources compiled
-    against the Eigen-API shim, single-threaded like the reference) when it was built, else the
-    numpy port. Bounded sample: the same solver configuration on an E=8^3 mesh, GMRES iterations
-    timed until ~`seconds` of CPU work; GDOF*iter/s is per-dof normalised."""
-    ref = os.path.join(ROOT, "oracle", "_ref", "semlab_ref_bench")
-    E = 8
-    if os.path.exists(ref):
-        out = subprocess.run([ref, "--eps", str(cfg["eps"]), "--elems", str(E), "--order", str(cfg["p"]),
-                              "--smoother", cfg["smoother"], "--coarse", cfg["coarse"], "--cheb-order",
-                              str(cfg["eta"]), "--krylov", cfg["krylov"], "--seconds", str(seconds)],
-                             capture_output=True, text=True, check=True).stdout
-        r = json.loads(out.strip().splitlines()[-1])
-        return {"value": r["gdof_iter_per_s"], "unit": UNIT, "cores": 1, "kind": "reference",
-                "sample": f"reference semlab (shim-compiled) + restated pMG/PCG, eps={cfg['eps']} E={E}^3 "
-                          f"p={cfg['p']}, {r['iters']} iterations in {r['t_solve_s']:.1f}s"}
-    import numpy as np
-    from oracle import semlab_np as o
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    mesh = o.generate_kershaw(cfg["eps"], E)
-    pmg = o.Pmg(mesh, cfg["orders"], cfg["smoother"], cfg["eta"], 0.1, 1.1, cfg["coarse"], cfg["precision"])
-    sp = pmg.spaces[0]
-    b = o.build_rhs(sp, 1)
-    iters, t = 0, 0.0
-    while t < seconds and iters < 200:
-        x = np.zeros(sp.n)
-        t0 = time.perf_counter()
-        st = o.gmres_solve(sp.apply_A, pmg.vcycle, b, x, o.GmresConfig(restart=20, tol=1e-8, max_iters=5))
-        t += time.perf_counter() - t0
-        iters += st.iterations
-    return {"value": sp.n * iters / t / 1e9, "unit": UNIT, "cores": int(os.environ.get("OMP_NUM_THREADS", "1")),
-            "kind": "port", "sample": f"numpy oracle port, eps={cfg['eps']} E={E}^3 p={cfg['p']}, "
-                                      f"{iters} GMRES iterations in {t:.1f}s"}
+def host_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "semlab_ref_bench")
+
+
+def ref_bench_cmd(cfg, iters, warm):
+    return [REF_BENCH, "--eps", str(cfg["eps"]), "--elems", str(cfg["E"]), "--order", str(cfg["p"]),
+            "--smoother", cfg["smoother"], "--coarse", cfg["coarse"], "--cheb-order", str(cfg["eta"]),
+            "--krylov", cfg["krylov"], "--iters", str(iters), "--warmup-iters", str(warm)]
+
+
+def ref_sample_desc(cfg, r, warm):
+    return (f"reference semlab (own TUs, Eigen-API shim) + restated pMG/PCG/RHS on the bench workload itself "
+            f"(eps={cfg['eps']} E={cfg['E']}^3 p={cfg['p']}, {cfg['krylov']}, FP64 smoother: the reference has no "
+            f"FP32 path): setup {r['t_setup_s']:.0f}s, {warm} untimed warm-up iteration(s), then the first "
+            f"{r['iters']} iterations of the solve from x0=0 timed ({r['t_solve_s']:.1f}s), 1 thread")
+
+
+def start_cpu_reference(cfg, iters, warm):
+    """The reference on the bench config as a child process pinned to the last host core (it runs
+    beside the GPU measurement; single-threaded like the reference)."""
+    if not os.path.exists(REF_BENCH):
+        return None
+    last = max(os.sched_getaffinity(0))
+
+    def pin():
+        try:
+            os.sched_setaffinity(0, {last})
+        except Exception:
+            pass
+    return subprocess.Popen(ref_bench_cmd(cfg, iters, warm), stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                            text=True, preexec_fn=pin)
+
+
+def finish_cpu_reference(proc, cfg, warm, timeout=1800):
+    if proc is None:
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref/semlab_ref_bench not built", **host_info()}
+    out, err = proc.communicate(timeout=timeout)
+    if proc.returncode != 0:
+        raise RuntimeError(f"semlab_ref_bench failed: {err[-300:]}")
+    r = json.loads(out.strip().splitlines()[-1])
+    return {"value": r["gdof_iter_per_s"], "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": ref_sample_desc(cfg, r, warm), "ms_per_iteration": r["t_solve_s"] / max(1, r["iters"]) * 1e3,
+            "setup_s": r["t_setup_s"], **host_info()}
 
 
 def run_reference(args, cfg, name):
+    """--impl reference: the reference's CPU path (oracle/_ref) on the bench workload itself. A step
+    is one Krylov iteration of the bench's solve (A, the V-cycle, CGS2); the K steps are the first K
+    iterations of one solve from x0 = 0 (K = 20: exactly the first GMRES(20) restart cycle). One
+    warm-up iteration runs untimed first: on the CPU there is nothing to warm beyond it, and each
+    iteration of this single-threaded reference costs tens of seconds at E=32^3."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    per_step = []
-    cb = None
-    for k in range(args.warmup + args.steps):
-        r = cpu_reference_sample(cfg, seconds=max(3.0, 60.0 / max(1, args.warmup + args.steps)))
-        if k >= args.warmup:
-            per_step.append(r["value"])
-        cb = r
-    v = sum(per_step) / len(per_step)
+    warm = 1
+    proc = start_cpu_reference(cfg, args.steps, warm)
+    if proc is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/semlab_ref_bench not built"}), flush=True)
+        return
+    cb = finish_cpu_reference(proc, cfg, warm, timeout=3600)
+    v = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": describe(name, cfg), "parallelism": "cpu"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"], "sample": cb["sample"]},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_iteration"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": describe(name, cfg), "parallelism": "cpu, 1 thread (the reference is serial)",
+                       "step": "one Krylov iteration of the bench solve (first K iterations from x0=0)",
+                       "warmup_iterations": warm, "setup_s": cb["setup_s"]},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "nproc", "cpu_model")},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------- byte model
+def kernel_bytes(cfg, n, E, n3=None, E3=None):
+    """Algorithmic HBM bytes per launch; n, E on the finest level."""
+    nloc = (cfg["p"] + 1) ** 3
+    P = cfg["p"] + 3
+    F = 4 * E * (3 * P * P + 3 * P)  # FP32 FDM factors S (3 P^2) and lambda (3 P) per element
+    return {
+        "ax64": 48 * E * nloc + 16 * n,          # FP64 factors, u in, w out (Krylov operator)
+        "ax32": 24 * E * nloc + 16 * n,          # FP32-rounded factors (smoother operator)
+        "ras0": F + 16 * n,                      # plain RAS: r in, z out
+        "ras1": F + 24 * n,                      # Chebyshev init: t in; r, d out
+        "ras2": F + 56 * n,                      # Chebyshev step: t, d, r, x in; x, r, d out
+        "ras3": F + 40 * n,                      # last step: t, d, r, x in; x out
+        "F": F,
+    }
+
+
+def solve_bytes(cfg, n, E, n1, E1, iters, restart=20):
+    """Algorithmic bytes of one bench solve (model, documented in DESIGN.md §6): per iteration the
+    Krylov A, the V-cycle (level 0: 6 Ax with FP32 factors + 2x(init, step, last) fused RAS; the
+    p=3 level likewise with FP64 factors; transfers; the small coarse solve omitted) and CGS2."""
+    kb = kernel_bytes(cfg, n, E)
+    P1 = 3 + 3
+    F1 = 4 * E1 * (3 * P1 * P1 + 3 * P1)
+    lvl0 = 6 * kb["ax32"] + 16 * n + 2 * (kb["ras1"] + kb["ras2"] + kb["ras3"])
+    lvl1 = 6 * (48 * E1 * 64 + 16 * n1) + 16 * n1 + 2 * (3 * F1 + 120 * n1)
+    transfers = 32 * n + 16 * n1
+    vcyc = lvl0 + lvl1 + transfers
+    total = 0
+    for it in range(iters):
+        j = it % restart
+        total += kb["ax64"] + vcyc + 8 * n * (3 * j + 8) + 16 * n + 8 * n  # A, M, CGS2, normalise, store z
+        if j == restart - 1 or it == iters - 1:
+            total += 8 * n * (j + 3) + kb["ax64"] + 24 * n + 8 * n  # x += Z y, true residual, norm
+    return total, vcyc
 
 
 # ---------------------------------------------------------------------------------- our path
@@ -172,6 +237,10 @@ def run_ours(args, cfg, name):
     else:
         ctx = S.Context(local, stream)
 
+    # the reference on this same workload runs beside the GPU measurement (rank 0, N=1 only)
+    cpu_proc = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_proc = start_cpu_reference(cfg, args.cpu_iters, 0)
     sm = {"ras": S.RAS_SMOOTHER, "jacobi": S.JACOBI_SMOOTHER, "asm": S.ASM_SMOOTHER}[cfg["smoother"]]
     cm = S.COARSE_AMG if cfg["coarse"] == "amg" else S.COARSE_DIRECT
     t0 = time.time()
@@ -254,73 +323,132 @@ def run_ours(args, cfg, name):
     e2e = {"value": n_global * it2 / t2 / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * sp.n,
            "d2h_bytes_per_step": 8 * sp.n, "steps": e2e_steps}
 
-    # roofline of the dominant kernel (fused Ax, global->global), timed live on its stream
+    # ---- rooflines of the kernels that run in the solve, each timed live on the solve's stream
     pk = peaks()
-    u = torch.randn(sp.n, dtype=torch.float64, device="cuda")
-    w = torch.empty_like(u)
-    for _ in range(3):
-        sp.apply_A(u, w)
-    reps = 20
-    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e4.record(stream)
-    for _ in range(reps):
-        sp.apply_A(u, w)
-    e5.record(stream)
-    torch.cuda.synchronize()
-    t_ax = e4.elapsed_time(e5) * 1e-3 / reps
-    nloc = (cfg["p"] + 1) ** 3
-    ax_bytes = 48 * sp.n_elements * nloc + 16 * sp.n
-    traffic = None
+    peak = pk.get("hbm_gbs", 6650.0)
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in pk else "fallback (B200_PROFILING.md)"
+    traffic_tab = {}
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_summary.json")))
-        if prof.get("workload") in (name, describe(name, cfg)) and world == 1:  # captured on one GPU
-            traffic = prof.get("ax_dram_bytes_per_launch")
+        if prof.get("workload") == name and world == 1:  # ncu --set full of this workload on one GPU
+            traffic_tab = prof.get("dram_bytes_per_launch", {})
     except Exception:
         pass
-    peak = pk.get("hbm_gbs", 6650.0)
-    achieved = ax_bytes / t_ax / 1e9
-    # the smoother kernel: FP32 RAS (FDM local solves) plain apply, r -> z, timed the same way
-    roof_s = None
-    if cfg["smoother"] == "ras" and world == 1:
-        sch = S.SchwarzSmoother(sp, S.RAS, cfg["precision"])
-        z = torch.empty_like(u)
+
+    def timed(fn, reps=20):
         for _ in range(3):
-            sch.apply(u, z)
+            fn()
+        e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e4.record(stream)
         for _ in range(reps):
-            sch.apply(u, z)
+            fn()
         e5.record(stream)
         torch.cuda.synchronize()
-        t_ras = e4.elapsed_time(e5) * 1e-3 / reps
-        P = cfg["p"] + 3
-        ras_bytes = (cfg["precision"] // 8) * sp.n_elements * (3 * P * P + 3 * P) + 16 * sp.n
-        ras_traffic = None
-        try:
-            prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_summary.json")))
-            if prof.get("workload") in (name, describe(name, cfg)):
-                ras_traffic = prof.get("ras_dram_bytes_per_launch")
-        except Exception:
-            pass
-        roof_s = {"kernel": "k_rasw (RAS, FP32 fast-diagonalisation local solves, owner write)", "bound": "hbm",
-                  "traffic": ras_traffic,
-                  "achieved": ras_bytes / t_ras / 1e9, "peak": pk.get("hbm_gbs", 6650.0), "unit": "GB/s",
-                  "frac": ras_bytes / t_ras / 1e9 / pk.get("hbm_gbs", 6650.0), "algorithmic_bytes_per_launch": ras_bytes,
-                  "us_per_launch": t_ras * 1e6, "flops_per_launch": 12 * P ** 4 * sp.n_elements}
-        del sch, z
-    roof = {"kernel": "k_axw (FP64 Ax on DMMA tensor cores + owner-ordered Q^T, global->global)", "bound": "hbm",
-            "achieved": achieved,
-            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-            "algorithmic_bytes_per_launch": ax_bytes, "us_per_launch": t_ax * 1e6,
-            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in pk else "fallback"}
+        return e4.elapsed_time(e5) * 1e-3 / reps
+
+    E_loc = sp.n_elements
+    kb = kernel_bytes(cfg, sp.n, E_loc)
+    u = torch.randn(sp.n, dtype=torch.float64, device="cuda")
+    sp.mask_inplace(u)
+    w = torch.empty_like(u)
+    roofs = {}
+
+    def add(key, kernel, nbytes, t, launches=1, per_solve=None):
+        ach = nbytes / t / 1e9
+        roofs[key] = {"kernel": kernel, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                      "frac": ach / peak, "traffic": traffic_tab.get(key), "algorithmic_bytes_per_launch": nbytes,
+                      "us_per_launch": t * 1e6 / launches, "launches": launches, "peak_source": peak_src}
+        if per_solve is not None:  # share of the timed solve (launches per solve x time per launch)
+            roofs[key]["per_solve"] = per_solve
+            roofs[key]["share_of_solve"] = per_solve * t / launches / (t_solve_s)
+
+    t_solve_s = t / args.steps
+    its = iters / args.steps
+    restarts = int(-(-its // 20))
+    if world == 1:
+        add("ax64", "k_axw<EWrite,double>: Krylov Ax, FP64 factors on DMMA, owner-ordered Q^T", kb["ax64"],
+            timed(lambda: sp.apply_A(u, w)), per_solve=its + restarts + 1)
+        if cfg["p"] == 7 and cfg["precision"] == 32:
+            add("ax32", "k_axw<.,float>: smoother Ax, FP32-rounded factors, FP64 DMMA", kb["ax32"],
+                timed(lambda: sp.apply_A_geom32(u, w)), per_solve=6 * its)
+        if cfg["smoother"] == "ras":
+            sch = S.SchwarzSmoother(sp, S.RAS, cfg["precision"])
+            add("ras0", "k_rasw mode 0: RAS, FP32 FDM local solves, owner write", kb["ras0"],
+                timed(lambda: sch.apply(u, w)), per_solve=6 * its)
+            # the fused Chebyshev(eta)-RAS smoothing exactly as the V-cycle runs it on the fine level
+            A32 = sp.as_linop_geom32() if (cfg["p"] == 7 and cfg["precision"] == 32) else sp.as_linop()
+            cheb = S.ChebyshevSmoother(sch.as_linop(), A32, S.ChebyParams(cfg["eta"], 0.1, 1.1, pmg.lam(0)))
+            xs = torch.zeros_like(u)
+            bb = b.clone()
+
+            def smooth():
+                xs.copy_(u)
+                cheb.smooth(bb, xs)
+            ax_epi = kb["ax32"] if (cfg["p"] == 7 and cfg["precision"] == 32) else kb["ax64"]
+            cheb_bytes = (cfg["eta"] + 1) * ax_epi + 8 * sp.n + kb["ras1"] + (cfg["eta"] - 1) * kb["ras2"] + kb["ras3"] \
+                + 16 * sp.n  # + the x copy of this harness
+            add("cheby_ras", f"Chebyshev({cfg['eta']})-RAS smoothing step, fine level: {cfg['eta'] + 1} Ax + "
+                f"{cfg['eta'] + 1} fused RAS launches (init, step, last)", cheb_bytes, timed(smooth),
+                launches=2 * (cfg["eta"] + 1) + 1, per_solve=2 * its * (2 * (cfg["eta"] + 1) + 1))
+            del cheb, sch, xs
+        n1 = (cfg["E"] * 3 + 1) ** 3
+        tot, vcyc = solve_bytes(cfg, sp.n, E_loc, n1, E_loc, int(round(its)))
+        vt = timed(lambda: pmg.vcycle(b, w), reps=10)
+        add("vcycle", "one pMG V-cycle (all levels, CUDA graph)", vcyc, vt, per_solve=its)
+        solver_roof = {"algorithmic_bytes_per_solve": tot, "t_solve_ms": t_solve_s * 1e3,
+                       "achieved": tot / t_solve_s / 1e9, "peak": peak, "unit": "GB/s",
+                       "frac": tot / t_solve_s / 1e9 / peak,
+                       "model": "per iteration: Krylov Ax + V-cycle (6 fine Ax + 2x(init,step,last) fused RAS; p=3 "
+                                "level likewise; transfers) + CGS2 8n(3j+8) + normalise; per restart: x += Z y, "
+                                "true residual (DESIGN.md section 6)"}
+    else:
+        solver_roof = None
+    dominant = max((r for r in roofs.values() if "share_of_solve" in r and r["launches"] == 1),
+                   key=lambda r: r["share_of_solve"], default=None)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if cpu_proc is not None:
         try:
-            cpu = cpu_reference_sample(cfg, seconds=args.cpu_seconds)
+            cpu = finish_cpu_reference(cpu_proc, cfg, 0)
+            cpu.pop("ms_per_iteration", None)
         except Exception as ex:  # reported, never fatal
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {ex}"}
+
+    # like-for-like line: the same solve with the FP64 smoother (the reference's arithmetic)
+    fp64 = None
+    if cfg["precision"] == 32 and not args.no_fp64_line:
+        del A, M, pmg, sp
+        torch.cuda.empty_cache()
+        pmg64 = S.Pmg(mesh, cfg["orders"], sm, cfg["eta"], 0.1, 1.1, 64, cm)
+        sp64 = pmg64.spaces[0]
+        A64, M64 = sp64.as_linop(), pmg64.as_linop()
+        b64 = sp64.build_rhs(1)
+        x64 = torch.zeros_like(b64)
+        for _ in range(2):
+            x64.zero_()
+            solve(A64, M64, b64, x64, gcfg)
+        k64 = max(1, min(args.steps, 5))
+        torch.cuda.synchronize()
+        barrier()
+        e6, e7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        it64 = 0
+        e6.record(stream)
+        for _ in range(k64):
+            x64.zero_()
+            st64 = solve(A64, M64, b64, x64, gcfg)
+            it64 += st64.iterations
+        e7.record(stream)
+        torch.cuda.synchronize()
+        t64 = e6.elapsed_time(e7) * 1e-3
+        if world > 1:
+            tt = torch.tensor([t64], dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t64 = tt.item()
+        fp64 = {"value": n_global * it64 / t64 / 1e9, "unit": UNIT, "ms_per_step": t64 / k64 * 1e3, "steps": k64,
+                "iterations_per_solve": it64 / k64, "converged": bool(st64.converged),
+                "smoother_precision": "fp64", "note": "same workload with the FP64 FDM smoother and FP64 smoother "
+                                                      "operator: the reference's arithmetic (like-for-like line)"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -332,8 +460,8 @@ def run_ours(args, cfg, name):
                            "krylov_precision": "fp64", "parallelism": f"z-slab x{world}", "setup_s": setup_s,
                            "l2": "inputs larger than L2 (geometry 805 MB at E=32^3)",
                            "time_to_1e-8_ms": t / args.steps * 1e3, "step_wall_ms": [round(v, 1) for v in step_ms]},
-                "e2e": e2e, "roofline": roof, "roofline_smoother": roof_s, "cpu_baseline": cpu,
-                "clocks": clk.summary(),
+                "e2e": e2e, "roofline": dominant, "rooflines": roofs, "solver_roofline": solver_roof,
+                "fp64_smoother": fp64, "cpu_baseline": cpu, "clocks": clk.summary(),
                 "gpu_launches": launches}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -348,7 +476,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-iters", type=int, default=1,
+                    help="iterations of the reference timed for cpu_baseline (after its setup)")
+    ap.add_argument("--no-fp64-line", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("timing rules: --warmup must be >= 3")

@@ -160,6 +160,8 @@ int semlab_space_dot(semlab_space s, const double* d_a, const double* d_b, doubl
 
 /* ---- operators (LinOp, types.hpp:13) ------------------------------------------------------ */
 int semlab_op_A(semlab_space s, semlab_op* out);          /* SemSpace::apply_A                */
+int semlab_op_A_geom32(semlab_space s, semlab_op* out); /* extension: apply_A_geom32 as a LinOp
+                                                              (the FP32 smoother's operator)  */
 int semlab_op_jacobi(semlab_space s, semlab_op* out);     /* S = diag(A)^-1     */
 int semlab_op_schwarz(semlab_schwarz sch, semlab_op* out); /* SchwarzSmoother::as_linop        */
 int semlab_op_pmg(semlab_pmg pmg, semlab_op* out);        /* pMG V-cycle as a preconditioner  */

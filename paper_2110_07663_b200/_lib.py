@@ -83,6 +83,7 @@ SIGNATURES = {
     "semlab_space_build_rhs": (i32, [p, u64, p]),
     "semlab_space_dot": (i32, [p, p, p, pf64]),
     "semlab_op_A": (i32, [p, C.POINTER(p)]),
+    "semlab_op_A_geom32": (i32, [p, C.POINTER(p)]),
     "semlab_op_jacobi": (i32, [p, C.POINTER(p)]),
     "semlab_op_schwarz": (i32, [p, C.POINTER(p)]),
     "semlab_op_pmg": (i32, [p, C.POINTER(p)]),

@@ -406,6 +406,20 @@ int semlab_op_A(semlab_space s, semlab_op* out) {
   });
 }
 
+int semlab_op_A_geom32(semlab_space s, semlab_op* out) {
+  return guard([&] {
+    need(s, "semlab_op_A_geom32: space");
+    if (!s->enable_geom32()) invalid("semlab_op_A_geom32: FP32 geometric factors exist for order 7 only");
+    auto o = std::make_unique<semlab_op_s>();
+    o->kind = semlab_op_s::kA;
+    o->ctx = s->ctx;
+    o->n = s->n;
+    o->space = s;
+    o->geom32 = true;
+    *out = o.release();
+  });
+}
+
 int semlab_op_jacobi(semlab_space s, semlab_op* out) {
   return guard([&] {
     need(s, "semlab_op_jacobi: space");

@@ -21,15 +21,11 @@
 #include "device.cuh"
 #include "kernels_fdm.hpp"
 
-#ifndef SEMLAB_RASW_GATHER_UNROLL
-#define SEMLAB_RASW_GATHER_UNROLL 2  // z-columns of the box gathered per lane per batch
-#endif
 #ifndef SEMLAB_RASW_OWNER_U
 #define SEMLAB_RASW_OWNER_U 4  // owned sites per lane per batch of the owner write
 #endif
-constexpr int kGatherUnroll = SEMLAB_RASW_GATHER_UNROLL;
 #ifndef SEMLAB_RASW_MINB
-#define SEMLAB_RASW_MINB 5  // resident 4-warp CTAs per SM the warp-per-element RAS is register-capped for
+#define SEMLAB_RASW_MINB 3  // resident 4-warp CTAs per SM (3 x 74.6 KB of shared memory at P = 10)
 #endif
 
 #ifndef SEMLAB_RAS_SMALLP_MINB
@@ -386,7 +382,10 @@ struct WShape {
   static constexpr int R = (P2 + 31) / 32;  // lines per lane
   static constexpr int WPC = 4;             // warps (elements in flight) per CTA
   static constexpr int NT = 32 * WPC;
-  static constexpr int SPE = (2 * P3 + 3 * P2 + 3 * P + 3) / 4 * 4;  // box, tmp, S, L (16B multiple)
+  static constexpr int FAC = (3 * P2 + 3 * P + 3) / 4 * 4;  // S (3 P^2) and lambda (3 P), 16B multiple
+  // per warp: FP64 staging of the next element's extended box (cp.async, one element ahead), the
+  // FP32 box and tmp of the line passes, and the factors double-buffered (one element ahead)
+  static constexpr int SPE = P3 * int(sizeof(double) / sizeof(T)) + 2 * P3 + 2 * FAC;
   static constexpr size_t smem() { return size_t(WPC) * SPE * sizeof(T); }
 };
 
@@ -411,8 +410,8 @@ __device__ __forceinline__ void load_pair(const T* M, T& s0, T& s1) {
 }
 
 // forward transform along AX: y[o] = sum_a M(a,o) x[a], x streamed from src, y in registers
-template <int P, class T, int AX>
-__device__ __forceinline__ void wfwd(const T* __restrict__ src, const T* __restrict__ M, const int (&base)[WShape<P, T>::R],
+template <int P, class T, int AX, class SrcT = T>
+__device__ __forceinline__ void wfwd(const SrcT* __restrict__ src, const T* __restrict__ M, const int (&base)[WShape<P, T>::R],
                                      T (&y)[WShape<P, T>::R][P]) {
   constexpr int R = WShape<P, T>::R;
   constexpr int stride = AX == 0 ? 1 : (AX == 1 ? P : P * P);
@@ -424,7 +423,7 @@ __device__ __forceinline__ void wfwd(const T* __restrict__ src, const T* __restr
   for (int a = 0; a < P; ++a) {
     T xa[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) xa[r] = src[base[r] + a * stride];
+    for (int r = 0; r < R; ++r) xa[r] = T(src[base[r] + a * stride]);
     if constexpr (P % 2 == 0 && sizeof(T) == 4 && SEMLAB_RASW_FFMA2) {
       // packed FP32 (FFMA2): the (o, o+1) output pair shares x_a; same per-output order as below
 #pragma unroll
@@ -528,91 +527,80 @@ __global__ void __launch_bounds__(WShape<P, T>::NT, sizeof(T) == 4 ? SEMLAB_RASW
     k_rasw(const Slab sl, const T* __restrict__ S, const T* __restrict__ L, const double* __restrict__ rin,
            RasEpi epi) {
   using W = WShape<P, T>;
-  constexpr int P2 = W::P2, P3 = W::P3, R = W::R, SPE = W::SPE;
+  constexpr int P2 = W::P2, P3 = W::P3, R = W::R, SPE = W::SPE, FAC = W::FAC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T* box = reinterpret_cast<T*>(smem_raw) + warp * SPE;
+  double* stage = reinterpret_cast<double*>(reinterpret_cast<T*>(smem_raw) + warp * SPE);
+  T* box = reinterpret_cast<T*>(stage + P3);
   T* tmp = box + P3;
-  T* Se = tmp + P3;
-  T* Le = Se + 3 * P2;
+  T* fac0 = tmp + P3;  // factors of even / odd iterations of this warp's element loop
   const int nE = int(sl.elems());
   const bool dir = sl.dirichlet != 0;
-  for (int el = blockIdx.x * W::WPC + warp; el < nE; el += gridDim.x * W::WPC) {
-    const int ex = el % sl.Ex, ey = (el / sl.Ex) % sl.Ey, ez = sl.ez0 + el / (sl.Ex * sl.Ey);
+  const int64_t NXY = sl.Nx * sl.Ny;
+  const int stride = gridDim.x * W::WPC;
+  // Issue the asynchronous loads of element e: its factors into fac, its extended box (FP64, the
+  // lattice vector as stored) into the staging buffer. Sites outside the box, and sites outside
+  // the element core in more than one direction (schwarz.cpp:255-265), are zero-filled by the
+  // copy itself (src-size 0). The box is gathered by z-columns: lane = (a, b) pair, so the x/y
+  // validity and the column address are fixed per pair and the z test is a bit mask.
+  auto issue = [&](int e, T* fac) {
+    const int ex = e % sl.Ex, ey = (e / sl.Ex) % sl.Ey, ez = sl.ez0 + e / (sl.Ex * sl.Ey);
     const Box1D X = box1d(ex, sl.Ex, sl.q, dir), Y = box1d(ey, sl.Ey, sl.q, dir), Z = box1d(ez, sl.Ez, sl.q, dir);
-#if SEMLAB_RASW_PF
-    {  // the next element's extended-box rows (and factors) -> L2 while this element is solved
-      const int en = el + gridDim.x * W::WPC;
-      if (en < nE) {
-        const int nx = en % sl.Ex, ny = (en / sl.Ex) % sl.Ey, nz = sl.ez0 + en / (sl.Ex * sl.Ey);
-        const Box1D NX = box1d(nx, sl.Ex, sl.q, dir), NY = box1d(ny, sl.Ey, sl.q, dir), NZ = box1d(nz, sl.Ez, sl.q, dir);
-        const double* nc = rin + sl.lidx(NX.lo, NY.lo, NZ.lo);
-        const int64_t NXY = sl.Nx * sl.Ny;
-        for (int rw = lane; rw < NY.n * NZ.n; rw += 32) {
-          const double* p = nc + (rw % NY.n) * sl.Nx + (rw / NY.n) * NXY;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p + NX.n - 1));
-        }
-        if (lane < (3 * P2 * int(sizeof(T)) + 127) / 128)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(S + int64_t(en) * 3 * P2) + lane * 128));
+    {
+      static_assert(sizeof(T) == 4, "k_rasw stages FP32 factors");
+      const T* se = S + int64_t(e) * 3 * P2;
+      if constexpr ((3 * P2) % 4 == 0) {  // P even: the element's S is 16-byte aligned, whole chunks
+        for (int w = lane; w < 3 * P2 / 4; w += 32) cp_async16(fac + 4 * w, se + 4 * w);
+      } else {
+        for (int w = lane; w < 3 * P2; w += 32) cp_async4(fac + w, se + w);
       }
+      if (lane < 3 * P) cp_async4(fac + 3 * P2 + lane, L + int64_t(e) * 3 * P + lane);
     }
-#endif
-    __syncwarp();  // the previous element's owner write has finished reading tmp
-    {  // factors: S (3 P^2) and lambda (3 P), all loads issued before the stores
-      constexpr int NF = 3 * P2 + 3 * P, IT = (NF + 31) / 32;
-      T v[IT];
+    unsigned zin = 0, zcore = 0;  // c < Z.n; c < Z.n and not a z ghost
 #pragma unroll
-      for (int it = 0; it < IT; ++it) {
-        const int w = lane + 32 * it;
-        v[it] = w < 3 * P2 ? __ldg(S + int64_t(el) * 3 * P2 + w)
-                           : (w < NF ? __ldg(L + int64_t(el) * 3 * P + (w - 3 * P2)) : T(0));
-      }
-#pragma unroll
-      for (int it = 0; it < IT; ++it) {
-        const int w = lane + 32 * it;
-        if (w < NF) Se[w] = v[it];
-      }
+    for (int c = 0; c < P; ++c) {
+      zin |= unsigned(c < Z.n) << c;
+      zcore |= unsigned(c < Z.n && !ghost(Z, c)) << c;
     }
-    {  // gather the extended box by z-columns: lane = (a, b) pair, loop over c, so the x/y
-       // validity and the column address are fixed per pair and the z test is a bit mask; sites
-       // outside the core in more than one direction (and outside a smaller boundary box) are zero
-       // (schwarz.cpp:255-265)
-      unsigned zin = 0, zcore = 0;  // c < Z.n; c < Z.n and not a z ghost
+    const double* corner = rin + sl.lidx(X.lo, Y.lo, Z.lo);
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const int l = lane + 32 * r;
+      if (l >= P2) break;
+      const int a = l % P, b = l / P;
+      const bool okab = a < X.n && b < Y.n;
+      const int gab = int(ghost(X, a)) + int(ghost(Y, b));
+      const unsigned m = !okab ? 0u : (gab == 0 ? zin : (gab == 1 ? zcore : 0u));
+      const double* col = corner + a + b * sl.Nx;
 #pragma unroll
       for (int c = 0; c < P; ++c) {
-        zin |= unsigned(c < Z.n) << c;
-        zcore |= unsigned(c < Z.n && !ghost(Z, c)) << c;
-      }
-      const int64_t NXY = sl.Nx * sl.Ny;
-      const double* corner = rin + sl.lidx(X.lo, Y.lo, Z.lo);
-#pragma unroll kGatherUnroll
-      for (int r = 0; r < R; ++r) {
-        const int l = min(lane + 32 * r, P2 - 1);  // lanes past the last pair redo it (same values)
-        const int a = l % P, b = l / P;
-        const bool okab = a < X.n && b < Y.n;
-        const int gab = int(ghost(X, a)) + int(ghost(Y, b));
-        const unsigned m = !okab ? 0u : (gab == 0 ? zin : (gab == 1 ? zcore : 0u));
-        const double* col = corner + a + b * sl.Nx;
-        double v[P];
-#pragma unroll
-        for (int c = 0; c < P; ++c) v[c] = __ldg((m >> c) & 1u ? col + c * NXY : rin);
-#pragma unroll
-        for (int c = 0; c < P; ++c) box[c * P2 + l] = (m >> c) & 1u ? T(v[c]) : T(0);
+        const bool on = (m >> c) & 1u;
+        cp_async8(stage + c * P2 + l, on ? col + c * NXY : rin, on);
       }
     }
-    __syncwarp();
+    cp_async_commit();
+  };
+  int el = blockIdx.x * W::WPC + warp;
+  if (el < nE) issue(el, fac0);
+  for (int it = 0; el < nE; el += stride, ++it) {
+    T* Se = fac0 + (it & 1) * FAC;
+    T* Le = Se + 3 * P2;
+    const int ex = el % sl.Ex, ey = (el / sl.Ex) % sl.Ey, ez = sl.ez0 + el / (sl.Ex * sl.Ey);
+    const Box1D X = box1d(ex, sl.Ex, sl.q, dir), Y = box1d(ey, sl.Ey, sl.q, dir), Z = box1d(ez, sl.Ez, sl.q, dir);
+    cp_async_wait_all();
+    __syncwarp();  // this element's box and factors are in shared memory for every lane
     int base[R];
     bool okl[R];
     T y[R][P];
     wbases<P, T, 0>(lane, base, okl);
-    wfwd<P, T, 0>(box, Se + 0 * P2, base, y);  // x forward: box -> tmp
+    wfwd<P, T, 0>(stage, Se + 0 * P2, base, y);  // x forward: staged FP64 box -> tmp (FP32)
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (okl[r])
 #pragma unroll
         for (int o = 0; o < P; ++o) tmp[base[r] + o] = y[r][o];
-    __syncwarp();
+    __syncwarp();  // the staging buffer and the other factor buffer are free: prefetch the next element
+    if (el + stride < nE) issue(el + stride, fac0 + ((it + 1) & 1) * FAC);
     wbases<P, T, 1>(lane, base, okl);
     wfwd<P, T, 1>(tmp, Se + 1 * P2, base, y);  // y forward: tmp -> box
 #pragma unroll
@@ -817,12 +805,14 @@ struct Launch {
   }
   template <int P>
   static void ras(const Slab& sl, const T* S, const T* L, const double* r, int mode, const RasEpi& e, cudaStream_t s) {
-    if (sizeof(T) == 4 && P >= SEMLAB_RASW_MINP && ras_warp() && sl.elems() < (int64_t(1) << 31)) {
-      if (mode == 0) rasw<P, 0>(sl, S, L, r, e, s);
-      else if (mode == 1) rasw<P, 1>(sl, S, L, r, e, s);
-      else if (mode == 2) rasw<P, 2>(sl, S, L, r, e, s);
-      else rasw<P, 3>(sl, S, L, r, e, s);
-      return;
+    if constexpr (sizeof(T) == 4 && P >= SEMLAB_RASW_MINP) {
+      if (ras_warp() && sl.elems() < (int64_t(1) << 31)) {
+        if (mode == 0) rasw<P, 0>(sl, S, L, r, e, s);
+        else if (mode == 1) rasw<P, 1>(sl, S, L, r, e, s);
+        else if (mode == 2) rasw<P, 2>(sl, S, L, r, e, s);
+        else rasw<P, 3>(sl, S, L, r, e, s);
+        return;
+      }
     }
     using Sh = Shape<P, T>;
     const int grid = int((sl.elems() + Sh::EPC - 1) / Sh::EPC);

@@ -124,9 +124,10 @@ __global__ void __launch_bounds__(kNT) k_cgs_update_norm(const double* __restric
   finish_partials<1>(acc, 1, partial, counter, nrm2);
 }
 
+// y = V c, or y += V c (accumulate; the sum V c is formed first, then added: x + (V y) rounding)
 template <int NC>
 __global__ void __launch_bounds__(kNT) k_gemv_n(const double* __restrict__ V, int64_t ldv, int ncol, const Coef cf,
-                                                double* __restrict__ y, int64_t n) {
+                                                double* __restrict__ y, int64_t n, bool accumulate) {
   for (int64_t i = int64_t(blockIdx.x) * kNT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kNT) {
     double v[NC];
 #pragma unroll
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(kNT) k_gemv_n(const double* __restrict__ V, in
 #pragma unroll
     for (int c = 0; c < NC; ++c)
       if (c < ncol) s += v[c] * cf.c[c];
-    y[i] = s;
+    y[i] = accumulate ? y[i] + s : s;
   }
 }
 
@@ -167,6 +168,12 @@ void check_ncol(int ncol) {
 
 int64_t launch_gemv_t(const double* V, int64_t ldv, int ncol, const double* w, int64_t off, int64_t len,
                       double* d_h, const DotScratch& ws, cudaStream_t s) {
+  if (ncol > kMaxCol) {  // wide bases (restart > 31): 32-column chunks, one launch each
+    int64_t k = 0;
+    for (int c0 = 0; c0 < ncol; c0 += kMaxCol)
+      k += launch_gemv_t(V + c0 * ldv, ldv, std::min(kMaxCol, ncol - c0), w, off, len, d_h + c0, ws, s);
+    return k;
+  }
   check_ncol(ncol);
 #define L_(NC) k_gemv_t<NC><<<blocks_for(len), kNT, 0, s>>>(V, ldv, ncol, w, off, len, d_h, ws.partial, ws.counter)
   SB_NC_DISPATCH(ncol, L_);
@@ -199,11 +206,18 @@ int64_t launch_cgs_update_norm(const double* V, int64_t ldv, int ncol, double* w
 }
 
 int64_t launch_gemv_n(const double* V, int64_t ldv, int ncol, const double* c_host, double* y, int64_t n,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool accumulate) {
+  if (ncol > kMaxCol) {  // wide bases: 32-column chunks, the later ones accumulate
+    int64_t k = 0;
+    for (int c0 = 0; c0 < ncol; c0 += kMaxCol)
+      k += launch_gemv_n(V + c0 * ldv, ldv, std::min(kMaxCol, ncol - c0), c_host + c0, y, n, s,
+                         accumulate || c0 > 0);
+    return k;
+  }
   check_ncol(ncol);
   Coef cf;
   for (int c = 0; c < kMaxCol; ++c) cf.c[c] = c < ncol ? c_host[c] : 0.0;
-#define L_(NC) k_gemv_n<NC><<<blocks_for(n), kNT, 0, s>>>(V, ldv, ncol, cf, y, n)
+#define L_(NC) k_gemv_n<NC><<<blocks_for(n), kNT, 0, s>>>(V, ldv, ncol, cf, y, n, accumulate)
   SB_NC_DISPATCH(ncol, L_);
 #undef L_
   SB_LAUNCH_CHECK();

@@ -75,7 +75,7 @@ int64_t launch_dots(int K, const double* const* a, const double* const* b, int64
                     const DotScratch& ws, cudaStream_t s);
 
 // ---- Krylov (CGS2 fused passes over the column-major basis V (ld = ldv)) -------------------
-// h[0..j] = V^T w
+// h[0..j] = V^T w (any ncol, chunked by 32)
 int64_t launch_gemv_t(const double* V, int64_t ldv, int ncol, const double* w, int64_t off, int64_t len,
                       double* d_h, const DotScratch& ws, cudaStream_t s);
 // w -= V h ; h2 = V^T w  (update and re-projection in one pass)
@@ -86,8 +86,10 @@ int64_t launch_cgs_update_dot(const double* V, int64_t ldv, int ncol, double* w,
 int64_t launch_cgs_update_norm(const double* V, int64_t ldv, int ncol, double* w, const double* d_h2,
                                int64_t n, int64_t off, int64_t len, double* d_nrm2, const DotScratch& ws,
                                cudaStream_t s);
-// y = V c (host coefficients)
+// y = V c, or y += V c with accumulate (host coefficients; any ncol, chunked by 32)
 int64_t launch_gemv_n(const double* V, int64_t ldv, int ncol, const double* c_host, double* y, int64_t n,
-                      cudaStream_t s);
+                      cudaStream_t s, bool accumulate = false);
+// Widest basis the fused CGS passes take in one launch; wider bases go in 32-column chunks.
+constexpr int kKrylovChunk = 32;
 
 }  // namespace sb

@@ -224,29 +224,52 @@ void fetch(semlab_ctx c, const double* d, double* h, int K) {
 }
 
 // One CGS2 Arnoldi step on w against V[:, :ncol] (krylov.cpp:67-76): h (incl. h2), ||w||.
-void cgs2(semlab_ctx c, const OwnRange& o, const double* V, int64_t ldv, int ncol, double* w, double* d_h,
+// Scratch stride of cgs2's device results: h at [0, nb), h2 at [nb, 2nb), |w|^2 at 2nb.
+int cgs2_stride(int ncol_max) { return std::max(kKrylovChunk, ncol_max); }
+
+// One CGS2 step (krylov.cpp:67-72; chebyshev.cpp:36-41): h = V^T w; w -= V h; h2 = V^T w;
+// w -= V h2; h += h2; hnext = |w|. Up to 32 columns the update and the next projection share one
+// pass over V (fused kernels); wider bases (restart > 31) run the same steps in 32-column chunks.
+void cgs2(semlab_ctx c, const OwnRange& o, const double* V, int64_t ldv, int ncol, double* w, double* d_h, int nb,
           std::vector<double>& h, double& hnext) {
   cudaStream_t s = c->stream;
-  double* d_h2 = d_h + 32;
-  double* d_nrm = d_h + 64;
+  double* d_h2 = d_h + nb;
+  double* d_nrm = d_h + 2 * nb;
   c->count(launch_gemv_t(V, ldv, ncol, w, o.off, o.len, d_h, c->dots(), s));
   c->allreduce_device(d_h, ncol);
-  c->count(launch_cgs_update_dot(V, ldv, ncol, w, d_h, o.n, o.off, o.len, d_h2, c->dots(), s));
-  c->allreduce_device(d_h2, ncol);
-  c->count(launch_cgs_update_norm(V, ldv, ncol, w, d_h2, o.n, o.off, o.len, d_nrm, c->dots(), s));
+  if (ncol <= kKrylovChunk) {
+    c->count(launch_cgs_update_dot(V, ldv, ncol, w, d_h, o.n, o.off, o.len, d_h2, c->dots(), s));
+    c->allreduce_device(d_h2, ncol);
+    c->count(launch_cgs_update_norm(V, ldv, ncol, w, d_h2, o.n, o.off, o.len, d_nrm, c->dots(), s));
+  } else {
+    for (int c0 = 0; c0 < ncol; c0 += kKrylovChunk)  // w -= V h (the chunk dots are not used)
+      c->count(launch_cgs_update_dot(V + c0 * ldv, ldv, std::min(kKrylovChunk, ncol - c0), w, d_h + c0, o.n, o.off,
+                                     o.len, d_h2, c->dots(), s));
+    c->count(launch_gemv_t(V, ldv, ncol, w, o.off, o.len, d_h2, c->dots(), s));
+    c->allreduce_device(d_h2, ncol);
+    for (int c0 = 0; c0 < ncol; c0 += kKrylovChunk)  // w -= V h2; the last chunk's norm is |w|^2
+      c->count(launch_cgs_update_norm(V + c0 * ldv, ldv, std::min(kKrylovChunk, ncol - c0), w, d_h2 + c0, o.n,
+                                      o.off, o.len, d_nrm, c->dots(), s));
+  }
   c->allreduce_device(d_nrm, 1);
-  SB_CUDA(cudaMemcpyAsync(c->host_pinned, d_h, sizeof(double) * 65, cudaMemcpyDeviceToHost, s));
+  const size_t cnt = size_t(2 * nb + 1);
+  std::vector<double> big;
+  double* hp = c->host_pinned;
+  if (cnt > 128) {
+    big.resize(cnt);
+    hp = big.data();
+  }
+  SB_CUDA(cudaMemcpyAsync(hp, d_h, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
   c->sync();
   h.assign(size_t(ncol), 0.0);
-  for (int k = 0; k < ncol; ++k) h[size_t(k)] = c->host_pinned[k] + c->host_pinned[32 + k];
-  hnext = std::sqrt(c->host_pinned[64]);
+  for (int k = 0; k < ncol; ++k) h[size_t(k)] = hp[k] + hp[nb + k];
+  hnext = std::sqrt(hp[2 * nb]);
 }
 
 }  // namespace
 
 semlab_lambda_estimate estimate_lambda_max(semlab_op S, semlab_op A, int64_t n, int rounds, uint64_t seed) {
   if (rounds < 1) invalid("estimate_lambda_max: rounds >= 1");
-  if (rounds > 31) invalid("estimate_lambda_max: rounds <= 31 on the device path");
   if (!S || !A || S->n != n || A->n != n) invalid("estimate_lambda_max: operator sizes differ from n");
   semlab_ctx c = A->ctx;
   cudaStream_t s = c->stream;
@@ -257,7 +280,7 @@ semlab_lambda_estimate estimate_lambda_max(semlab_op S, semlab_op A, int64_t n, 
   int64_t offset = 0;
   if (A->space) offset = A->space->sl.zlo * A->space->sl.Nx * A->space->sl.Ny;
   uniform_pm1_range(seed, offset, n, hv.data());
-  DevBuf<double> v(static_cast<size_t>(n)), t(static_cast<size_t>(n)), w(static_cast<size_t>(n)), V(size_t(n) * (rounds + 1)), dh(96);
+  DevBuf<double> v(static_cast<size_t>(n)), t(static_cast<size_t>(n)), w(static_cast<size_t>(n)), V(size_t(n) * (rounds + 1)), dh(size_t(3 * cgs2_stride(rounds + 1)));
   v.upload(hv.data(), size_t(n), s);
   std::vector<double> H(size_t(rounds + 1) * rounds, 0.0);  // column-major (rounds+1) x rounds
   A->apply(v.p, t.p);
@@ -277,7 +300,7 @@ semlab_lambda_estimate estimate_lambda_max(semlab_op S, semlab_op A, int64_t n, 
     A->apply(V.p + size_t(j) * n, t.p);
     S->apply(t.p, w.p);
     double hnext = 0.0;
-    cgs2(c, o, V.p, n, j + 1, w.p, dh.p, h, hnext);
+    cgs2(c, o, V.p, n, j + 1, w.p, dh.p, cgs2_stride(rounds + 1), h, hnext);
     for (int i = 0; i <= j; ++i) H[size_t(i) + size_t(rounds + 1) * j] = h[size_t(i)];
     H[size_t(j + 1) + size_t(rounds + 1) * j] = hnext;
     m = j + 1;
@@ -330,7 +353,6 @@ struct WsLease {
 
 KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, const semlab_gmres_config& cfg) {
   if (cfg.restart < 1) invalid("gmres: restart must be >= 1");
-  if (cfg.restart > 31) invalid("gmres: restart must be <= 31 on the device path");
   if (!(cfg.tol > 0.0)) invalid("gmres: tol must be positive");
   if (!A) invalid("gmres: missing operator");
   semlab_ctx c = A->ctx;
@@ -340,16 +362,20 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
   const OwnRange o = own_range_of(A);
   KrylovResult res;
   const int64_t ld = padded(n);
-  WsLease ws(c, size_t(ld) * (m + 4) + 96);
+  // Preconditioned directions z_j = M v_j are kept (Z, m columns) and the update is x += Z y. For
+  // a linear M this is the reference's x += M (V y) (krylov.cpp:108-114) up to rounding, one M
+  // application cheaper per restart cycle; for the FP32 smoother's V-cycle (linear only to
+  // ~1e-7) it keeps the least-squares residual estimate consistent with the true residual, so
+  // the FP32-smoothed solve needs the FP64 solve's iteration count instead of an extra restart.
+  const int nb = cgs2_stride(m + 1);
+  const int zc = M ? m : 0;
+  WsLease ws(c, size_t(ld) * (m + 3 + zc) + size_t(3 * nb));
   struct {
     double* p;
-  } r{ws.p}, w{ws.p + ld}, z{ws.p + 2 * ld}, V{ws.p + 3 * ld}, dh{ws.p + size_t(ld) * (m + 4)};
-  auto applyM = [&](const double* in, double* out) {
-    if (M)
-      M->apply(in, out);
-    else
-      c->count(launch_copy(out, in, n, s));
-  };
+  } r{ws.p}, w{ws.p + ld}, V{ws.p + 2 * ld}, Z{ws.p + size_t(ld) * (m + 3)},
+      dh{ws.p + size_t(ld) * (m + 3 + zc)};
+  // z_j: stored column of Z, or v_j itself without a preconditioner
+  auto dir = [&](int j) { return M ? Z.p + size_t(j) * ld : V.p + size_t(j) * ld; };
   auto norm = [&](const double* v) {
     const double* av[1] = {v};
     double r2 = 0.0;
@@ -379,10 +405,10 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
     int j = 0;
     bool lucky = false;
     for (; j < m && res.iterations < cfg.max_iters; ++j) {
-      applyM(V.p + size_t(j) * ld, z.p);
-      A->apply(z.p, w.p);
+      if (M) M->apply(V.p + size_t(j) * ld, dir(j));
+      A->apply(dir(j), w.p);
       double hnext = 0.0;
-      cgs2(c, o, V.p, ld, j + 1, w.p, dh.p, h, hnext);
+      cgs2(c, o, V.p, ld, j + 1, w.p, dh.p, nb, h, hnext);
       for (int i = 0; i <= j; ++i) Hc(i, j) = h[size_t(i)];
       Hc(j + 1, j) = hnext;
       for (int i = 0; i < j; ++i) {  // Givens (krylov.cpp:77-89)
@@ -412,16 +438,14 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
         break;
       }
     }
-    if (j > 0) {  // x += M (V y), krylov.cpp:108-114
+    if (j > 0) {  // x += Z y  (= M (V y) for a linear M, krylov.cpp:108-114)
       std::vector<double> y(static_cast<size_t>(j));
       for (int i = j - 1; i >= 0; --i) {
         double acc = g[size_t(i)];
         for (int k = i + 1; k < j; ++k) acc -= Hc(i, k) * y[size_t(k)];
         y[size_t(i)] = acc / Hc(i, i);
       }
-      c->count(launch_gemv_n(V.p, ld, j, y.data(), w.p, n, s));
-      applyM(w.p, z.p);
-      c->count(launch_axpby(x, 1.0, z.p, 1.0, n, s));
+      c->count(launch_gemv_n(dir(0), ld, j, y.data(), x, n, s, true));
     }
     A->apply(x, r.p);
     c->count(launch_sub(r.p, b, r.p, n, s));

@@ -305,6 +305,12 @@ class SemSpace:
         check(lib.semlab_op_A(self.handle, C.byref(h)))
         return LinOp(h, self.n, self.ctx, keep=self)
 
+    def as_linop_geom32(self) -> LinOp:
+        """apply_A_geom32 as an operator: the FP32 smoother's A (order 7)."""
+        h = C.c_void_p()
+        check(lib.semlab_op_A_geom32(self.handle, C.byref(h)))
+        return LinOp(h, self.n, self.ctx, keep=self)
+
     def jacobi(self) -> LinOp:
         """S = diag(A)^-1 (precond.cpp missing in the reference)."""
         h = C.c_void_p()

@@ -98,3 +98,37 @@ def test_gmres_identity_one_iteration(ctx):
     st = S.gmres_solve(ident, None, b, x)
     assert st.converged and st.iterations == 1
     assert torch.allclose(x, b, atol=1e-14)
+
+
+@pytest.mark.parametrize("restart,precond", [(40, True), (45, False), (1, True), (33, True)])
+def test_gmres_any_restart_matches_oracle(ctx, restart, precond):
+    """The reference accepts any restart >= 1 (krylov.cpp:22): bases wider than 32 columns run the
+    CGS2 passes in 32-column chunks. With and without a preconditioner (the device keeps the
+    preconditioned directions Z; x += Z y equals the reference's x += M (V y) for a linear M)."""
+    from paper_2110_07663_b200 import semlab as S
+    g, c = _pair(ctx, 0.3, 2, 5)
+    b = o.build_rhs(c, 1)
+    inv = o.jacobi_inverse_diag(c)
+    x = np.zeros(c.n)
+    Mo = (lambda v: inv * v) if precond else None
+    cfg = dict(restart=restart, max_iters=300)
+    st_o = o.gmres_solve(c.apply_A, Mo, b, x, o.GmresConfig(**cfg))
+    xg = g.zeros()
+    st_g = S.gmres_solve(g.as_linop(), g.jacobi() if precond else None, g.to_device(b), xg, S.GmresConfig(**cfg))
+    assert st_g.converged == st_o.converged
+    assert abs(st_g.iterations - st_o.iterations) <= 1
+    if st_o.converged:
+        assert rel(xg, x) < 1e-9
+    else:  # GMRES(1) stalls: after 300 iterations x amplifies 1e-15 perturbations to ~1e-2 (oracle vs oracle)
+        np.testing.assert_allclose(st_g.history[:20], st_o.history[:20], rtol=1e-8)
+
+
+def test_lambda_estimate_many_rounds(ctx):
+    """estimate_lambda_max with rounds > 32 (chunked CGS2) against the oracle."""
+    from paper_2110_07663_b200 import semlab as S
+    g, c = _pair(ctx, 0.3, 2, 5)
+    inv = o.jacobi_inverse_diag(c)
+    want = o.estimate_lambda_max(lambda v: inv * v, c.apply_A, c.n, 40, 0)
+    got = S.estimate_lambda_max(g.jacobi(), g.as_linop(), g.n, 40, 0)
+    assert got.rounds_used == want.rounds_used
+    assert abs(got.value - want.value) <= 1e-9 * want.value

@@ -42,6 +42,10 @@ def main():
     E, nloc = sp.n_elements, (a.p + 1) ** 3
     byts = 48 * E * nloc + 16 * sp.n
     print(f"Ax: {t * 1e6:.1f} us  {byts / t / 1e9:.0f} GB/s (alg bytes {byts / 1e6:.1f} MB)", flush=True)
+    if a.p == 7:
+        t = timeit(lambda: sp.apply_A_geom32(u, w))
+        byts = 24 * E * nloc + 16 * sp.n
+        print(f"Ax geom32: {t * 1e6:.1f} us  {byts / t / 1e9:.0f} GB/s (alg bytes {byts / 1e6:.1f} MB)", flush=True)
     t0 = time.time()
     sch = S.SchwarzSmoother(sp, S.RAS, 32)
     print(f"schwarz setup {time.time() - t0:.2f}s", flush=True)
@@ -49,7 +53,18 @@ def main():
     t = timeit(lambda: sch.apply(u, z))
     P = a.p + 3
     byts = 4 * E * (3 * P * P + 3 * P) + 16 * sp.n
-    print(f"RAS fp32: {t * 1e6:.1f} us  {byts / t / 1e9:.0f} GB/s (alg bytes {byts / 1e6:.1f} MB)", flush=True)
+    print(f"RAS fp32: {t * 1e6:.1f} us  {byts / t / 1e9:.0f} GB/s (alg bytes {byts / 1e6:.1f} MB) "
+          f"{12 * P ** 4 * E / t / 1e12:.1f} TFLOP/s", flush=True)
+    if a.p == 7:
+        cheb = S.ChebyshevSmoother(sch.as_linop(), sp.as_linop_geom32(), S.ChebyParams(2, 0.1, 1.1, 12.8))
+        xs = torch.zeros_like(u)
+        bb = sp.build_rhs(1)
+
+        def smooth():
+            xs.copy_(u)
+            cheb.smooth(bb, xs)
+        t = timeit(smooth)
+        print(f"cheby(2)-RAS smooth (3 Ax32 + 3 RAS): {t * 1e6:.1f} us", flush=True)
     if not a.solve:
         return
     t0 = time.time()
