@@ -9,8 +9,9 @@
 // Workload: the bench configuration itself (same mesh, order, schedule, smoother, coarse solve,
 // Krylov method, b = build_rhs(seed 1), x0 = 0). After setup, --warmup-iters Krylov iterations
 // run untimed (a separate solve call), then ONE solve call limited to --iters iterations is
-// timed: for GMRES(20) with --iters 20 that is exactly the first restart cycle of the bench's
-// solve (Arnoldi steps with A, the V-cycle and CGS2, then x += M(Vy) and the true residual).
+// timed: the first --iters Arnoldi steps of the bench's solve (A, the V-cycle, CGS2), less one
+// separately timed M + A application for the cycle close the solve call adds.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -65,9 +66,21 @@ int main(int argc, char** argv) {
   const auto ts = clk::now();
   const GmresStats st = solve(iters);
   const double t = std::chrono::duration<double>(clk::now() - ts).count();
-  std::printf("{\"n\": %ld, \"iters\": %d, \"t_solve_s\": %.6f, \"t_setup_s\": %.3f, \"t_warmup_s\": %.3f, "
-              "\"rel_residual\": %.6e, \"gdof_iter_per_s\": %.9g}\n",
-              long(s.n()), st.iterations, t, t_setup, t_warm, st.rel_residual,
-              double(s.n()) * double(st.iterations) / t / 1e9);
+  // A solve call also runs the restart-cycle close: x += M (V y) and the true residual b - A x
+  // (krylov.cpp:108-118), one M and one A application. Timed separately here and taken out, so
+  // the rate is per Arnoldi iteration (A, M, CGS2) of the timed solve.
+  double t_close = 0.0;
+  if (krylov == "gmres") {
+    FieldVector z(s.n()), w(s.n());
+    const auto tc = clk::now();
+    M(b, z);
+    A(z, w);
+    t_close = std::chrono::duration<double>(clk::now() - tc).count();
+  }
+  const double t_iter = std::max(t - t_close, 1e-9);
+  std::printf("{\"n\": %ld, \"iters\": %d, \"t_solve_s\": %.6f, \"t_close_s\": %.6f, \"t_setup_s\": %.3f, "
+              "\"t_warmup_s\": %.3f, \"rel_residual\": %.6e, \"gdof_iter_per_s\": %.9g}\n",
+              long(s.n()), st.iterations, t, t_close, t_setup, t_warm, st.rel_residual,
+              double(s.n()) * double(st.iterations) / t_iter / 1e9);
   return 0;
 }

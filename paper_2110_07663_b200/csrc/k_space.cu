@@ -696,25 +696,52 @@ int64_t axp_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
   return 1;
 }
 
+struct Cands {  // elements (along one axis) containing a lattice coordinate, ascending
+  int n;
+  int e[2];
+  int loc[2];
+};
+__device__ __forceinline__ Cands cands(int64_t c, int q, int Eax, int lo_elem, int hi_elem) {
+  // hi_elem = one past the last element layer available locally
+  Cands r;
+  int64_t e = c / q;
+  const int l = int(c % q);
+  if (l == 0 && e > 0) {
+    r.n = 0;
+    if (e - 1 >= lo_elem) { r.e[r.n] = int(e - 1); r.loc[r.n] = q; ++r.n; }
+    if (e < hi_elem) { r.e[r.n] = int(e); r.loc[r.n] = 0; ++r.n; }
+  } else {
+    if (e == Eax) { e -= 1; }
+    r.n = 1;
+    r.e[0] = int(e);
+    r.loc[0] = (e * q == c) ? 0 : int(c - e * q);
+  }
+  return r;
+}
+
 // ------------------------------------------------------------------------ warp-per-element Ax (p = 7)
-// The p=7 operator on the FP64 tensor cores. Every contraction of sem_space.cpp:137-174 is a
-// stack of 8x8x8 products, i.e. two mma.m8n8k4.f64 (DMMA) each:
-//   ur_k = U_k D^T, us_k = D U_k (per z-layer k), ut_(.,j,.) = D U_(.,j,.) (per y-row j),
-//   out_k = Gr_k D + D^T Gs_k (+) D^T Gt_(.,j,.)
-// so an element costs 96 DMMA instead of 2 x 384 DFMA warp-instructions, and the kernel is no
-// longer issue-bound. One warp owns one element at a time (no CTA barriers: __syncwarp only);
-// the warp loops over dynamic tickets in ascending element id and implements Q^T with the same
-// owner protocol and summation order as k_ax/k_axp (deposits, per-element release counters,
-// face-owned nodes finished one ticket later). A lane holds the nodes (k = 0..7, j = lane/4,
-// i = 2(lane%4) + {0,1}), the D-fragments live in 4 registers, and the per-warp shared
-// workspace (3 arrays of 8 z-layers) is padded and XOR-swizzled so every fragment access is
-// conflict-free (2 wavefronts per 256 B).
-#ifndef SEMLAB_AXW_TMA
-#define SEMLAB_AXW_TMA 0  // whole-element geometry by one TMA bulk copy into shared memory, one element ahead
-#endif
+// The p=7 operator on the FP64 tensor cores, in two launches with no inter-CTA waiting:
+//
+// k_axe: one warp per element (grid-stride, static order). Every contraction of
+//   sem_space.cpp:137-174 is a stack of 8x8x8 products, i.e. two mma.m8n8k4.f64 (DMMA) each:
+//     ur_k = U_k D^T, us_k = D U_k (per z-layer k), ut_(.,j,.) = D U_(.,j,.) (per y-row j),
+//     out_k = Gr_k D + D^T Gs_k (+) D^T Gt_(.,j,.)
+//   so an element costs 96 DMMA. A lane holds the nodes (k = 0..7, j = lane/4, i = 2(lane%4) +
+//   {0,1}), the D fragments live in 4 registers, and the per-warp shared workspace (3 arrays of
+//   8 z-layers) is padded and XOR-swizzled so every fragment access is conflict-free. The 216
+//   interior nodes of the element have a single contributor: their epilogue (plain write,
+//   residual, or the whole Chebyshev-Jacobi update) is applied right here. The 296 face nodes
+//   go to a compact per-element face buffer (E x 296 doubles, 78 MB at E=32^3: written and read
+//   back through L2). The next element's geometry and u rows are prefetched to L2 while this
+//   one is computed, so every warp keeps a whole element of loads in flight.
+// k_face_epi7: one thread per lattice node on an element face sums its 2-8 contributions from
+//   the face buffer in ASCENDING element id (the order of the reference gather,
+//   sem_space.cpp:40-52, 110-119), applies the Dirichlet mask and the epilogue. Results are
+//   bitwise those of the one-kernel owner-ordered protocol this replaces, and deterministic.
 namespace axw {
 constexpr int PS = 72;  // z-layer stride (doubles): 64 + 8 so consecutive layers use opposite bank halves
 constexpr int ARR = 8 * PS;
+constexpr int FACE = 296;  // face nodes of a p=7 element: 2 x 64 (k = 0, 7) + 6 x 28 (rings)
 __device__ __forceinline__ int sidx(int k, int j, int i) {  // swizzled workspace index
   return k * PS + j * 8 + 2 * ((i >> 1) ^ ((j >> 1) & 3)) + (i & 1);
 }
@@ -723,28 +750,25 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
+// compact index of a face node (i, j, k) of an 8^3 element (at least one coordinate is 0 or 7)
+__device__ __forceinline__ int face_idx(int i, int j, int k) {
+  if (k == 0) return j * 8 + i;
+  if (k == 7) return 64 + j * 8 + i;
+  const int b = 128 + (k - 1) * 28;
+  if (j == 0) return b + i;
+  if (j == 7) return b + 8 + i;
+  return b + 16 + 2 * (j - 1) + (i == 7 ? 1 : 0);
+}
 }  // namespace axw
 
 #ifndef SEMLAB_AXW_WARPS
-#define SEMLAB_AXW_WARPS (SEMLAB_AXW_TMA ? 1 : 4)  // warps (independent element pipelines) per CTA
-#endif
-#ifndef SEMLAB_AXW_GPF
-#define SEMLAB_AXW_GPF 2  // geometry L2 prefetch: 0 none, 1 one element ahead, 2 current element, 3 bulk (current)
-#endif
-#ifndef SEMLAB_AXW_PDEP
-#define SEMLAB_AXW_PDEP 1  // face-owned results wait in the element's deposit slots, not registers
+#define SEMLAB_AXW_WARPS 4  // warps (independent element pipelines) per CTA
 #endif
 #ifndef SEMLAB_AXW_MINB
-#define SEMLAB_AXW_MINB (SEMLAB_AXW_TMA ? 5 : 3)  // resident CTAs per SM
-#endif
-#ifndef SEMLAB_AXW_MINB_F
-#define SEMLAB_AXW_MINB_F SEMLAB_AXW_MINB  // the same for the FP32-factor (smoother) operator
+#define SEMLAB_AXW_MINB 3  // resident CTAs per SM
 #endif
 
-template <class GT>
-__host__ __device__ constexpr int axw_warp_doubles() {  // per-warp shared memory in doubles
-  return 3 * axw::ARR + (SEMLAB_AXW_TMA ? 6 * 512 * int(sizeof(GT)) / 8 : 0);
-}
+__host__ __device__ constexpr int axw_warp_doubles() { return 3 * axw::ARR; }  // per-warp shared memory in doubles
 
 __device__ __forceinline__ double2 ld_geom2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ double2 ld_geom2(const float* p) {
@@ -752,30 +776,19 @@ __device__ __forceinline__ double2 ld_geom2(const float* p) {
   return make_double2(double(v.x), double(v.y));
 }
 
-__device__ __forceinline__ double2 ld_geom2_smem(const double* p) { return *reinterpret_cast<const double2*>(p); }
-__device__ __forceinline__ double2 ld_geom2_smem(const float* p) {
-  const float2 v = *reinterpret_cast<const float2*>(p);
-  return make_double2(double(v.x), double(v.y));
-}
-
 // GT = double: the operator itself (Krylov A). GT = float: the smoother's operator with the
 // geometric factors rounded to FP32 (half the bytes; arithmetic stays FP64 on the DMMA path).
 template <class EpiT, class GT>
-__global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLAB_AXW_MINB_F : SEMLAB_AXW_MINB)
-    k_axw(const Slab sl, const DMat<8> Dm, const double* __restrict__ u, const GT* __restrict__ geom,
-          double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int total_tickets,
-          const EpiT epi) {
+__global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
+    k_axe(const Slab sl, const DMat<8> Dm, const double* __restrict__ u, const GT* __restrict__ geom,
+          double* __restrict__ fb, const EpiT epi) {
   using namespace axw;
   constexpr int ND = 8, ND2 = 64, NLOC = 512, q = 7;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* sU = reinterpret_cast<double*>(smem_raw) + size_t(wid) * axw_warp_doubles<GT>();  // u, then Gr
-  double* sS = sU + ARR;                                                                 // Gs
-  double* sT = sS + ARR;                                                                 // ut, Gt, then D^T Gt
-  GT* sGeo = reinterpret_cast<GT*>(sT + ARR);  // SEMLAB_AXW_TMA: the element's 6 factor planes
-  uint64_t* gbar = reinterpret_cast<uint64_t*>(smem_raw + size_t(SEMLAB_AXW_WARPS) * axw_warp_doubles<GT>() * 8) + wid;
-  constexpr unsigned GBYTES = 6 * 512 * sizeof(GT);
-  unsigned gphase = 0;
+  double* sU = reinterpret_cast<double*>(smem_raw) + size_t(wid) * axw_warp_doubles();  // u, then Gr
+  double* sS = sU + ARR;                                                               // Gs
+  double* sT = sS + ARR;                                                               // ut, Gt, then D^T Gt
   const int gj = lane >> 2, gc = lane & 3;  // fragment row / column group
   const int j = gj, i0 = 2 * gc;            // this lane's nodes: (k, j, i0 + {0,1})
   // D fragments: Df[kc] = D(lane/4, lane%4 + 4kc), Dt[kc] = D(lane%4 + 4kc, lane/4)
@@ -789,29 +802,13 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
   const int Ex = sl.Ex, Ey = sl.Ey, LZ = Ex * Ey;
   const int Nx = int(sl.Nx), Ny = int(sl.Ny), Nz = int(sl.Nz), NxNy = Nx * Ny;
   const int zlo = int(sl.zlo);
+  const int stride = gridDim.x * SEMLAB_AXW_WARPS;
 
-  auto take = [&]() {
-    int t = 0;
-    if (lane == 0) {
-      t = int(atomicAdd(ticket, 1u));
-      if (t == total_tickets - 1) atomicExch(ticket, 0u);
-    }
-    return __shfl_sync(0xffffffffu, t, 0);
-  };
-  auto prefetch_geom = [&](int e) {  // element e's geometry (24 KB FP64 / 12 KB FP32) -> L2
+  auto prefetch = [&](int e) {  // element e's geometry (24 KB FP64 / 12 KB FP32) and u rows -> L2
     const char* gb = reinterpret_cast<const char*>(geom + size_t(e) * 6 * NLOC);
     constexpr int GL = 6 * NLOC * int(sizeof(GT)) / 128 / 32;  // 128-byte lines per lane
-    if (SEMLAB_AXW_GPF == 3) {  // one bulk (TMA engine) L2 prefetch
-      if (lane == 0)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gb), "r"(6 * NLOC * int(sizeof(GT))) : "memory");
-    } else {
 #pragma unroll
-      for (int l = 0; l < GL; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(gb + (l * 32 + lane) * 128));
-    }
-  };
-  auto prefetch = [&](int e) {  // element e's u rows (and geometry, SEMLAB_AXW_GPF=1) -> L2
-    if (e >= nE) return;
-    if (SEMLAB_AXW_GPF == 1) prefetch_geom(e);
+    for (int l = 0; l < GL; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(gb + (l * 32 + lane) * 128));
     const int ex = e % Ex, ey = (e / Ex) % Ey, ez = sl.ez0 + e / LZ;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
@@ -822,112 +819,10 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
     }
   };
 
-  int el = take();
-  if (el >= nE) return;
-  const unsigned target = *reinterpret_cast<volatile unsigned*>(&flags[el]) + 1u;
-  if (SEMLAB_AXW_TMA && lane == 0) {  // this element's geometry -> shared memory (TMA engine)
-    mbar_init(gbar, 1);
-    mbar_expect_tx(gbar, GBYTES);
-    bulk_g2s(sGeo, geom + size_t(el) * 6 * NLOC, GBYTES, gbar);
-  }
-  int prev = -1;
-#if !SEMLAB_AXW_PDEP
-  double pprev[16];  // face-owned results of ticket t-1 ([k][i - i0])
-#pragma unroll
-  for (int t = 0; t < 16; ++t) pprev[t] = 0.0;
-#endif
-
-  auto finish_prev = [&](int pe) {
-    const int ex = pe % Ex, ey = (pe / Ex) % Ey, ez = sl.ez0 + pe / LZ;
-    if (lane < 7) {  // wait for the <= 7 lower neighbours of pe (released long ago, normally)
-      const int a = (lane + 1) & 1, b = ((lane + 1) >> 1) & 1, c = ((lane + 1) >> 2) & 1;
-      if ((!a || ex > 0) && (!b || ey > 0) && (!c || ez > sl.ez0)) {
-        const int nb = pe - a - b * Ex - c * LZ;
-        while (ld_relaxed(&flags[nb]) < target) {
-        }
-      }
-    }
-    __syncwarp();
-    const bool hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
-    const bool owny = (j < q) || (ey == Ey - 1);
-    const bool topz = (ez == sl.ez1 - 1);
-    const int y = ey * q + j, zb = ez * q;
-    const bool mz0 = sl.dirichlet && zb == 0, mzq = sl.dirichlet && zb + q == Nz - 1;
-    const bool my = sl.dirichlet && (y == 0 || y == Ny - 1);
-    const double* db = dep + size_t(pe) * NLOC + j * ND;
-    const int oX = NLOC, oY = Ex * NLOC, oZ = LZ * NLOC;
-    // all predicated deposit loads of a 4-layer batch for both of this lane's columns are in
-    // flight together (two L2 round trips per element)
-    const int x0 = ex * q + i0;
-    const bool hx0 = (i0 == 0 && ex > 0);
-    const bool ownx1 = (i0 + 1 < q) || (ex == Ex - 1);
-    const int g0 = x0 + Nx * y + NxNy * (zb - zlo);
-    const bool mx[2] = {my || (sl.dirichlet && (x0 == 0 || x0 == Nx - 1)), my || (sl.dirichlet && (x0 + 1 == Nx - 1))};
-    const bool ownxy[2] = {owny, ownx1 && owny};  // i0 is even, so i0 < q
-    const bool hx[2] = {hx0, false};
-    const double* d = db + i0;
-    double cz[2], cxz[2], cyz[2], cxyz[2];
-#pragma unroll
-    for (int ii = 0; ii < 2; ++ii) {
-      const bool own0 = ownxy[ii] && hz;
-      cxyz[ii] = ldcg_pred(d + ii - (oZ + oY + oX) + q * ND2 + q * ND + q, own0 && hx[ii] && hy);
-      cyz[ii] = ldcg_pred(d + ii - (oZ + oY) + q * ND2 + q * ND, own0 && hy);
-      cxz[ii] = ldcg_pred(d + ii - (oZ + oX) + q * ND2 + q, own0 && hx[ii]);
-      cz[ii] = ldcg_pred(d + ii - oZ + q * ND2, own0);
-    }
-#pragma unroll
-    for (int kb = 0; kb < ND; kb += 4) {
-      double cx[4][2], cy[4][2], cxy[4][2];
-#if SEMLAB_AXW_PDEP
-      double cs[4][2];  // the element's own face-owned results, parked in its deposit slots
-#endif
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = kb + kk;
-#pragma unroll
-        for (int ii = 0; ii < 2; ++ii) {
-          const bool own = ownxy[ii] && (k < q || topz);
-          cxy[kk][ii] = ldcg_pred(d + ii - (oX + oY) + k * ND2 + q * ND + q, own && hx[ii] && hy);
-          cy[kk][ii] = ldcg_pred(d + ii - oY + k * ND2 + q * ND, own && hy);
-          cx[kk][ii] = ldcg_pred(d + ii - oX + k * ND2 + q, own && hx[ii]);
-#if SEMLAB_AXW_PDEP
-          cs[kk][ii] = ldcg_pred(d + ii + k * ND2, own && (hx[ii] || hy || (k == 0 && hz)));
-#endif
-        }
-      }
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = kb + kk;
-#pragma unroll
-        for (int ii = 0; ii < 2; ++ii) {
-          if (!(ownxy[ii] && (k < q || topz))) continue;
-          if (!(hx[ii] || hy || (k == 0 && hz))) continue;  // interior-owned: already written
-          double acc = 0.0;
-          if (k == 0) {  // (c=1): (b,a) = (1,1), (1,0), (0,1), (0,0)
-            acc += cxyz[ii];
-            acc += cyz[ii];
-            acc += cxz[ii];
-            acc += cz[ii];
-          }
-          acc += cxy[kk][ii];  // (c=0): (1,1), (1,0), (0,1), then the element itself
-          acc += cy[kk][ii];
-          acc += cx[kk][ii];
-#if SEMLAB_AXW_PDEP
-          acc += cs[kk][ii];
-#else
-          acc += pprev[k * 2 + ii];
-#endif
-          const bool m = mx[ii] || (k == 0 && mz0) || (k == q && mzq);
-          epi(g0 + k * NxNy + ii, m ? 0.0 : acc);
-        }
-      }
-    }
-  };
-
-  int nxt = take();
-  while (true) {
-    if (!SEMLAB_AXW_TMA && SEMLAB_AXW_GPF >= 2) prefetch_geom(el);
-    prefetch(nxt);
+  int el = blockIdx.x * SEMLAB_AXW_WARPS + wid;
+  if (el < nE) prefetch(el);
+  for (; el < nE; el += stride) {
+    if (el + stride < nE) prefetch(el + stride);
     const int ex = el % Ex, ey = (el / Ex) % Ey, ez = sl.ez0 + el / LZ;
     const int y = ey * q + j, zb = ez * q;
     const int xb = ex * q + i0;
@@ -936,7 +831,8 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
     const bool mx0 = my || (sl.dirichlet && (xb == 0 || xb == Nx - 1));
     const bool mx1 = my || (sl.dirichlet && (xb + 1 == Nx - 1));
     const bool mz0 = sl.dirichlet && zb == 0, mzq = sl.dirichlet && zb + q == Nz - 1;
-    // u: this lane's 16 nodes -> swizzled workspace
+    __syncwarp();  // the previous element's workspace reads are done
+    // u: this lane's 16 nodes (masked, sem_space.cpp:199) -> swizzled workspace
     {
       double v[16];
 #pragma unroll
@@ -951,8 +847,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
         *reinterpret_cast<double2*>(sU + sidx(k, j, i0)) = make_double2(a, b);
       }
     }
-    __syncwarp();  // also orders every lane's deposits of ticket t-1 before lane 0's release
-    if (prev >= 0 && lane == 0) st_release(&flags[prev], target);
+    __syncwarp();
     // ut: per y-row jj, (k, i) <- D (k, m) U(m, jj, i)
 #pragma unroll
     for (int jj = 0; jj < ND; ++jj) {
@@ -965,24 +860,15 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
     // per z-layer: ur, us (DMMA), ut (workspace), geometric factors, then Gr/Gs/Gt back out
     const GT* ge = geom + size_t(el) * 6 * NLOC + j * ND + i0;
     double2 gA[6], gB[6];
-    if (SEMLAB_AXW_TMA) {
-      mbar_wait(gbar, gphase);
-      gphase ^= 1u;
-    } else {
 #pragma unroll
-      for (int c = 0; c < 6; ++c) gA[c] = ld_geom2(ge + c * NLOC);
-    }
+    for (int c = 0; c < 6; ++c) gA[c] = ld_geom2(ge + c * NLOC);
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       double2* gcur = (k & 1) ? gB : gA;
       double2* gnext = (k & 1) ? gA : gB;
-      if (SEMLAB_AXW_TMA) {
+      if (k + 1 < ND) {
 #pragma unroll
-        for (int c = 0; c < 6; ++c) gcur[c] = ld_geom2_smem(sGeo + c * NLOC + k * ND2 + j * ND + i0);
-      } else if (k + 1 < ND) {
-#pragma unroll
-        for (int c = 0; c < 6; ++c)
-          gnext[c] = ld_geom2(ge + c * NLOC + (k + 1) * ND2);
+        for (int c = 0; c < 6; ++c) gnext[c] = ld_geom2(ge + c * NLOC + (k + 1) * ND2);
       }
       double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -1010,11 +896,6 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
       *reinterpret_cast<double2*>(sT + sidx(k, j, i0)) = make_double2(gt[0], gt[1]);
     }
     __syncwarp();
-    if (SEMLAB_AXW_TMA && lane == 0 && nxt < nE) {  // the next element's geometry streams in now
-      fence_proxy_async_shared();
-      mbar_expect_tx(gbar, GBYTES);
-      bulk_g2s(sGeo, geom + size_t(nxt) * 6 * NLOC, GBYTES, gbar);
-    }
     // out_k = Gr_k D + D^T Gs_k
     double o[16];
 #pragma unroll
@@ -1043,52 +924,82 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, sizeof(GT) == 4 ? SEMLA
       o[2 * k] += t2.x;
       o[2 * k + 1] += t2.y;
     }
-    // epilogue: deposit non-owned, finish interior-owned now, keep face-owned in registers
+    // epilogue: interior nodes (one contributor) now, face nodes to the face buffer
     {
-      const bool owny = (j < q) || (ey == Ey - 1);
-      const bool topz = (ez == sl.ez1 - 1);
-      const bool hy = (j == 0 && ey > 0), hz = (ez > sl.ez0);
-      double* dl = dep + size_t(el) * NLOC + j * ND + i0;
+      const bool jface = (j == 0 || j == q);
+      double* fe = fb + size_t(el) * FACE;
 #pragma unroll
       for (int kb = 0; kb < ND; kb += 4) {
         typename EpiT::In in[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          const int k = kb + t / 2, ii = t % 2, i = i0 + ii;
-          const bool own = ((i < q) || (ex == Ex - 1)) && owny && (k < q || topz);
-          const bool hx = (i == 0 && ex > 0);
-          if (own && !(hx || hy || (k == 0 && hz))) in[t] = epi.load(g0 + k * NxNy + ii);
+          const int k = kb + t / 2, i = i0 + t % 2;
+          const bool face = jface || k == 0 || k == q || i == 0 || i == q;
+          if (!face) in[t] = epi.load(g0 + k * NxNy + t % 2);
         }
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          const int k = kb + t / 2, ii = t % 2, i = i0 + ii;
-          const bool own = ((i < q) || (ex == Ex - 1)) && owny && (k < q || topz);
-          const bool hx = (i == 0 && ex > 0);
-          const double v = o[2 * k + ii];
-          if (!own || (SEMLAB_AXW_PDEP && (hx || hy || (k == 0 && hz)))) {
-            dl[k * ND2 + ii] = v;  // deposit (or, face-owned, park until the neighbours are in)
-          } else if (!(hx || hy || (k == 0 && hz))) {
-            const bool m = (ii ? mx1 : mx0) || (k == 0 && mz0) || (k == q && mzq);
-            epi.store(g0 + k * NxNy + ii, in[t], m ? 0.0 : v);
-          }
+          const int k = kb + t / 2, i = i0 + t % 2;
+          const bool face = jface || k == 0 || k == q || i == 0 || i == q;
+          const double v = o[2 * k + t % 2];
+          if (face)
+            fe[face_idx(i, j, k)] = v;
+          else
+            epi.store(g0 + k * NxNy + t % 2, in[t], v);
         }
       }
     }
-    // the release of this element is deferred until the next element's u has been gathered
-    // (its MEMBAR then finds the deposits long acknowledged instead of stalling the warp)
-    if (prev >= 0) finish_prev(prev);
-#if !SEMLAB_AXW_PDEP
-#pragma unroll
-    for (int t = 0; t < 16; ++t) pprev[t] = o[t];
-#endif
-    prev = el;
-    el = nxt;
-    if (el >= nE) break;
-    nxt = take();
   }
-  __syncwarp();
-  if (lane == 0) st_release(&flags[prev], target);
-  finish_prev(prev);
+}
+
+// Face nodes of the slab: (a) planes z % q == 0, (b) z % q != 0 with y % q == 0, (c) z, y % q != 0
+// with x % q == 0. Each sums its contributors' face-buffer entries in ascending element id.
+template <class EpiT>
+__global__ void __launch_bounds__(256) k_face_epi7(const Slab sl, const double* __restrict__ fb, const EpiT epi) {
+  using namespace axw;
+  constexpr int q = 7;
+  const int64_t Nx = sl.Nx, Ny = sl.Ny;
+  const int nzl = sl.ez1 - sl.ez0;               // element layers on this rank
+  const int64_t na = int64_t(nzl + 1) * Nx * Ny;  // (a)
+  const int64_t nb = int64_t(nzl) * (q - 1) * (sl.Ey + 1) * Nx;          // (b)
+  const int64_t nc = int64_t(nzl) * (q - 1) * (int64_t(sl.Ey) * (q - 1)) * (sl.Ex + 1);  // (c)
+  const int64_t total = na + nb + nc;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    int64_t x, y, z;
+    if (t < na) {
+      x = t % Nx;
+      y = (t / Nx) % Ny;
+      z = int64_t(sl.ez0) * q + (t / (Nx * Ny)) * q;
+    } else if (t < na + nb) {
+      const int64_t s = t - na;
+      x = s % Nx;
+      y = ((s / Nx) % (sl.Ey + 1)) * q;
+      const int64_t zz = s / (Nx * (sl.Ey + 1));  // 0 .. nzl (q-1) - 1
+      z = int64_t(sl.ez0) * q + (zz / (q - 1)) * q + 1 + zz % (q - 1);
+    } else {
+      const int64_t s = t - na - nb;
+      x = (s % (sl.Ex + 1)) * q;
+      const int64_t yy = (s / (sl.Ex + 1)) % (int64_t(sl.Ey) * (q - 1));
+      y = (yy / (q - 1)) * q + 1 + yy % (q - 1);
+      const int64_t zz = s / ((sl.Ex + 1) * (int64_t(sl.Ey) * (q - 1)));
+      z = int64_t(sl.ez0) * q + (zz / (q - 1)) * q + 1 + zz % (q - 1);
+    }
+    const int64_t g = sl.lidx(x, y, z);
+    if (sl.masked(x, y, z)) {
+      epi(g, 0.0);
+      continue;
+    }
+    const Cands cx = cands(x, q, sl.Ex, 0, sl.Ex), cy = cands(y, q, sl.Ey, 0, sl.Ey);
+    const Cands cz = cands(z, q, sl.Ez, sl.ez0, sl.ez1);
+    double acc = 0.0;
+    for (int c = 0; c < cz.n; ++c)
+      for (int b = 0; b < cy.n; ++b)
+        for (int a = 0; a < cx.n; ++a) {
+          const int64_t el = cx.e[a] + int64_t(sl.Ex) * (cy.e[b] + int64_t(sl.Ey) * (cz.e[c] - sl.ez0));
+          acc += fb[el * FACE + face_idx(cx.loc[a], cy.loc[b], cz.loc[c])];
+        }
+    epi(g, acc);
+  }
 }
 
 template <class EpiT, class GT>
@@ -1100,14 +1011,17 @@ int64_t axw_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
   if (sl.n_local() >= (int64_t(1) << 31) || nE * NLOC >= (int64_t(1) << 31))
     invalid("SemSpace: a rank's lattice must have < 2^31 nodes");
   constexpr int W = SEMLAB_AXW_WARPS;
-  const size_t smem = size_t(W) * axw_warp_doubles<GT>() * sizeof(double) + size_t(W) * 8;
-  auto kern = k_axw<EpiT, GT>;
+  const size_t smem = size_t(W) * axw_warp_doubles() * sizeof(double);
+  auto kern = k_axe<EpiT, GT>;
   const int nctas = resident_ctas(kern, 32 * W, smem);
   const int grid = capped_grid(std::min<int64_t>(nctas, (nE + W - 1) / W));
-  kern<<<grid, 32 * W, smem, s>>>(sl, dmat<8>(sl.q), u, geom, sy.dep, sy.flags, sy.ticket, int(nE + int64_t(grid) * W),
-                                   epi);
+  kern<<<grid, 32 * W, smem, s>>>(sl, dmat<8>(sl.q), u, geom, sy.dep, epi);
   SB_LAUNCH_CHECK();
-  return 1;
+  const int64_t nzl = sl.ez1 - sl.ez0;
+  const int64_t faces = (nzl + 1) * sl.Nx * sl.Ny + nzl * 6 * (sl.Ey + 1) * sl.Nx + nzl * 6 * (sl.Ey * 6) * (sl.Ex + 1);
+  k_face_epi7<<<capped_grid(std::min<int64_t>((faces + 255) / 256, 148 * 16)), 256, 0, s>>>(sl, sy.dep, epi);
+  SB_LAUNCH_CHECK();
+  return 2;
 }
 
 bool ax_dmma() {  // SEMLAB_AX_DMMA=0 selects the FP64-FMA persistent kernel (A/B measurement)
@@ -1116,29 +1030,6 @@ bool ax_dmma() {  // SEMLAB_AX_DMMA=0 selects the FP64-FMA persistent kernel (A/
     return !(e && e[0] == '0');
   }();
   return on;
-}
-
-struct Cands {  // elements (along one axis) containing a lattice coordinate, ascending
-  int n;
-  int e[2];
-  int loc[2];
-};
-__device__ __forceinline__ Cands cands(int64_t c, int q, int Eax, int lo_elem, int hi_elem) {
-  // hi_elem = one past the last element layer available locally
-  Cands r;
-  int64_t e = c / q;
-  const int l = int(c % q);
-  if (l == 0 && e > 0) {
-    r.n = 0;
-    if (e - 1 >= lo_elem) { r.e[r.n] = int(e - 1); r.loc[r.n] = q; ++r.n; }
-    if (e < hi_elem) { r.e[r.n] = int(e); r.loc[r.n] = 0; ++r.n; }
-  } else {
-    if (e == Eax) { e -= 1; }
-    r.n = 1;
-    r.e[0] = int(e);
-    r.loc[0] = (e * q == c) ? 0 : int(c - e * q);
-  }
-  return r;
 }
 
 // Q^T of element-local results with an owner epilogue: each lattice node sums its <= 8
