@@ -204,6 +204,9 @@ int semlab_pmg_destroy(semlab_pmg p);
 int semlab_pmg_vcycle(semlab_pmg p, const double* d_b, double* d_z);
 /* fine-level space handle (owned by the hierarchy) */
 int semlab_pmg_space(semlab_pmg p, int level, semlab_space* out);
+/* Coarse AMG hierarchy (SEMLAB_COARSE_AMG): number of levels and the row count of each (up to
+   cap), like AmgHierarchy::n_levels / level_size (amg.hpp:39-40); 0 levels for the direct solve. */
+int semlab_pmg_coarse_info(semlab_pmg p, int* nlevels, int64_t* sizes, int cap);
 /* lambda estimate used at a level */
 int semlab_pmg_lambda(semlab_pmg p, int level, double* out);
 /* P (coarse level+1 -> level) and P^T, device vectors of the two levels' spaces. */

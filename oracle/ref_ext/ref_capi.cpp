@@ -386,4 +386,21 @@ int ref_case_solve(void* h, int krylov, int restart, double tol, int max_iters, 
   });
 }
 
+// AMG hierarchy of the p=1 coarse problem (CoarseSolve "amg"): level sizes and the level-0
+// aggregate of every free dof (tests compare the product's hierarchy against it).
+int ref_amg_info(double eps, int E, int* nlev, int64_t* sizes, int cap, int* agg0) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, 1);
+    SemSpace s(m, 1);
+    CoarseSolve cs(s, "amg");
+    const AmgHierarchy* h = cs.amg();
+    *nlev = h->n_levels();
+    for (int l = 0; l < h->n_levels() && l < cap; ++l) sizes[l] = h->level_size(l);
+    if (agg0 && h->n_levels() > 1) {
+      const auto& a = h->aggregates(0);
+      for (size_t i = 0; i < a.size(); ++i) agg0[i] = a[i];
+    }
+  });
+}
+
 }  // extern "C"

@@ -31,6 +31,7 @@ class CoarseSolve {
  public:
   CoarseSolve(const semlab::SemSpace& s, const std::string& mode);
   semlab::FieldVector solve(const semlab::FieldVector& r) const;
+  const semlab::AmgHierarchy* amg() const { return amg_.get(); }
 
  private:
   const semlab::SemSpace* sp;

@@ -104,6 +104,7 @@ SIGNATURES = {
     "semlab_pmg_vcycle": (i32, [p, p, p]),
     "semlab_pmg_space": (i32, [p, i32, C.POINTER(p)]),
     "semlab_pmg_lambda": (i32, [p, i32, pf64]),
+    "semlab_pmg_coarse_info": (i32, [p, pi32, pi64, i32]),
     "semlab_pmg_prolong": (i32, [p, i32, p, p]),
     "semlab_pmg_restrict": (i32, [p, i32, p, p]),
     "semlab_gmres_solve": (i32, [p, p, p, p, C.POINTER(GmresConfigC), C.POINTER(GmresStatsC)]),

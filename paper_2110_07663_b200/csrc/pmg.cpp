@@ -24,6 +24,77 @@ double HostCsr::coeff(int64_t i, int64_t j) const {
   return (it != e && *it == int(j)) ? val[size_t(it - idx.data())] : 0.0;
 }
 
+// Geometric factors of every element computed on the host exactly as the reference does
+// (sem_space.cpp:58-97: J by D-contractions of the nodal coordinates, det and inverse by 3x3
+// cofactors, G = (w det) (J^-1 J^-T) formed like Eigen's eager product), in plain IEEE double
+// without FMA contraction. The coarse matrix is then bitwise the reference's, and so is its AMG
+// hierarchy: aggregation breaks ties on exact comparisons (|a_ij| >= theta max, w > best,
+// amg.cpp:17-52), so ulp-level differences in the entries (e.g. from the device k_geom, which
+// fuses multiply-adds) would change aggregates. Layout as the device geometry: SoA per element.
+static std::vector<double> host_geometry(semlab_space sp) {
+  const int q = sp->order, nd = q + 1, nl = nd * nd * nd;
+  const int64_t E = sp->E;
+  const Slab& sl = sp->sl;
+  const Gll& g = gll(q);
+  const double* D = g.diff.data();  // D(i, m) = D[i + nd m]
+  const double* W = g.weights.data();
+  std::vector<double> geom(size_t(E) * 6 * nl);
+  for (int64_t el = 0; el < E; ++el) {
+    const int ex = int(el % sl.Ex), ey = int((el / sl.Ex) % sl.Ey), ez = sl.ez0 + int(el / (int64_t(sl.Ex) * sl.Ey));
+    auto X = [&](int i, int j, int k, int c) {
+      const int64_t gl = sl.lidx(int64_t(ex) * q + i, int64_t(ey) * q + j, int64_t(ez) * q + k);
+      return sp->coords[size_t(gl) * 3 + size_t(c)];
+    };
+    for (int k = 0; k < nd; ++k)
+      for (int j = 0; j < nd; ++j)
+        for (int i = 0; i < nd; ++i) {
+          double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+          for (int m = 0; m < nd; ++m)
+            for (int c = 0; c < 3; ++c) {
+              J[c][0] += D[i + nd * m] * X(m, j, k, c);
+              J[c][1] += D[j + nd * m] * X(i, m, k, c);
+              J[c][2] += D[k + nd * m] * X(i, j, m, c);
+            }
+          const double det = J[0][0] * (J[1][1] * J[2][2] - J[2][1] * J[1][2]) -
+                             J[1][0] * (J[0][1] * J[2][2] - J[2][1] * J[0][2]) +
+                             J[2][0] * (J[0][1] * J[1][2] - J[1][1] * J[0][2]);
+          if (!(det > 0.0)) numeric("SemSpace: non-positive Jacobian in element " + std::to_string(el));
+          const double w = W[i] * W[j] * W[k];
+          const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], c10 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
+                       c20 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+          const double idet = 1.0 / (J[0][0] * c00 + J[0][1] * c10 + J[0][2] * c20);
+          double Ji[3][3];
+          Ji[0][0] = c00 * idet;
+          Ji[1][0] = c10 * idet;
+          Ji[2][0] = c20 * idet;
+          Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * idet;
+          Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * idet;
+          Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * idet;
+          Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * idet;
+          Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * idet;
+          Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * idet;
+          // P = Ji Ji^T column by column, l ascending, zero factors skipped (the eager product)
+          double P[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+          for (int cj = 0; cj < 3; ++cj)
+            for (int l = 0; l < 3; ++l) {
+              const double b = Ji[cj][l];
+              if (b == 0.0) continue;
+              for (int r = 0; r < 3; ++r) P[r][cj] += Ji[r][l] * b;
+            }
+          const double s = w * det;
+          const int node = i + nd * (j + nd * k);
+          double* ge = geom.data() + size_t(el) * 6 * nl + node;
+          ge[0 * nl] = s * P[0][0];
+          ge[1 * nl] = s * P[0][1];
+          ge[2 * nl] = s * P[0][2];
+          ge[3 * nl] = s * P[1][1];
+          ge[4 * nl] = s * P[1][2];
+          ge[5 * nl] = s * P[2][2];
+        }
+  }
+  return geom;
+}
+
 // Element matrices from the reference kernel applied to unit vectors (sem_space.cpp:127-175),
 // assembled like setFromTriplets (duplicates summed in insertion order: ascending element).
 HostCsr assemble_free_matrix(semlab_space sp) {
@@ -31,13 +102,10 @@ HostCsr assemble_free_matrix(semlab_space sp) {
   if (sp->distributed()) invalid("coarse solve: assemble on a whole-mesh space");
   const int q = sp->order, nd = q + 1, nl = nd * nd * nd, nd2 = nd * nd;
   const int64_t E = sp->E;
-  std::vector<double> geom(size_t(E) * 6 * nl);
-  SB_CUDA(cudaMemcpyAsync(geom.data(), sp->geom.p, geom.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                          sp->ctx->stream));
-  sp->ctx->sync();
   const Gll& g = gll(q);
   const double* D = g.diff.data();
   const Slab& sl = sp->sl;
+  std::vector<double> geom = host_geometry(sp);
   const int64_t fx = sl.Nx - 2, fy = sl.Ny - 2, fz = sl.Nz - 2;
   const int64_t nfree = fx * fy * fz;
   std::vector<std::vector<std::pair<int, double>>> rows(static_cast<size_t>(nfree));
@@ -697,6 +765,16 @@ int semlab_pmg_space(semlab_pmg p, int level, semlab_space* out) {
     need(p, "pmg: hierarchy");
     if (level < 0 || level >= int(p->lv.size())) invalid("pmg: level out of range");
     *out = p->lv[size_t(level)].sp;
+  });
+}
+
+int semlab_pmg_coarse_info(semlab_pmg p, int* nlevels, int64_t* sizes, int cap) {
+  return guard([&] {
+    need(p, "pmg: hierarchy");
+    need(nlevels, "pmg_coarse_info: nlevels");
+    const auto& lev = p->coarse.lev;
+    *nlevels = int(lev.size());
+    for (int l = 0; l < int(lev.size()) && l < cap; ++l) sizes[l] = lev[size_t(l)].n;
   });
 }
 

@@ -425,6 +425,13 @@ class Pmg:
         check(lib.semlab_pmg_lambda(self.handle, level, C.byref(v)))
         return v.value
 
+    def coarse_levels(self) -> list:
+        """Row counts of the coarse AMG hierarchy's levels (AmgHierarchy::level_size)."""
+        nl = C.c_int()
+        sizes = (C.c_int64 * 64)()
+        check(lib.semlab_pmg_coarse_info(self.handle, C.byref(nl), sizes, 64))
+        return [int(sizes[i]) for i in range(nl.value)]
+
     def vcycle(self, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         out = torch.empty_like(b) if out is None else out
         check(lib.semlab_pmg_vcycle(self.handle, _ptr(b), _ptr(out)))

@@ -97,6 +97,24 @@ def run(name):
           f"({os.path.getsize(path) / 1e6:.2f} MB)", flush=True)
 
 
+def amg_sizes():
+    """Level sizes of the reference AMG hierarchy of the p=1 coarse problem (CoarseSolve "amg"):
+    aggregation breaks ties on exact comparisons, so these pin the coarse matrix bitwise."""
+    import json
+    lib = C.CDLL(LIB)
+    out = {}
+    for eps in (0.3, 1.0):
+        for E in (4, 8, 16, 32):
+            nl, sizes = C.c_int(), (C.c_int64 * 32)()
+            if lib.ref_amg_info(C.c_double(eps), E, C.byref(nl), sizes, 32, None) != 0:
+                raise RuntimeError("ref_amg_info failed")
+            out[f"e{eps}_E{E}"] = [int(sizes[i]) for i in range(nl.value)]
+    path = os.path.join(HERE, "amg_levels.json")
+    json.dump(out, open(path, "w"), indent=1)
+    print(f"wrote {path}: {out}")
+
+
 if __name__ == "__main__":
-    for nm in sys.argv[1:] or list(sc.CASES):
-        run(nm)
+    args = sys.argv[1:] or list(sc.CASES) + ["amg"]
+    for nm in args:
+        amg_sizes() if nm == "amg" else run(nm)

@@ -174,3 +174,18 @@ def test_solve_fp32_smoother_at_scale(ctx, case):
     assert st.converged
     assert abs(st.iterations - it_ref) <= 1
     assert err <= 1e-6
+
+
+@pytest.mark.parametrize("eps,E", [(0.3, 8), (0.3, 16), (0.3, 32), (1.0, 16), (1.0, 32)])
+def test_coarse_amg_hierarchy_matches_reference(ctx, eps, E):
+    """The p=1 coarse matrix is assembled bitwise like the reference's (host geometry as
+    sem_space.cpp:58-97, element column probes, setFromTriplets order), so the aggregation, which
+    breaks ties on exact comparisons (amg.cpp:17-52), builds the reference's own hierarchy: every
+    level has the reference's size (tests/golden/amg_levels.json, from oracle/_ref)."""
+    import json
+    from paper_2110_07663_b200 import semlab as S
+    want = json.load(open(os.path.join(HERE, "golden", "amg_levels.json")))[f"e{eps}_E{E}"]
+    pmg = S.Pmg(S.generate_kershaw(eps, E, ctx), (3, 1), S.JACOBI_SMOOTHER, 2, 0.1, 1.1, 64, S.COARSE_AMG)
+    got = pmg.coarse_levels()
+    print(f"eps={eps} E={E}: product {got} reference {want}")
+    assert got == want
