@@ -21,11 +21,15 @@
 #include "device.cuh"
 #include "kernels_fdm.hpp"
 
+#ifndef SEMLAB_RASW_GATHER_UNROLL
+#define SEMLAB_RASW_GATHER_UNROLL 2  // z-columns of the box gathered per lane per batch
+#endif
 #ifndef SEMLAB_RASW_OWNER_U
 #define SEMLAB_RASW_OWNER_U 4  // owned sites per lane per batch of the owner write
 #endif
+constexpr int kGatherUnroll = SEMLAB_RASW_GATHER_UNROLL;
 #ifndef SEMLAB_RASW_MINB
-#define SEMLAB_RASW_MINB 3  // resident 4-warp CTAs per SM (3 x 74.6 KB of shared memory at P = 10)
+#define SEMLAB_RASW_MINB 5  // resident 4-warp CTAs per SM the warp-per-element RAS is register-capped for
 #endif
 
 #ifndef SEMLAB_RAS_SMALLP_MINB
@@ -373,277 +377,335 @@ __global__ void __launch_bounds__(128, ras_minb<P, T>()) k_ras(const Slab sl, co
 // Same arithmetic (and summation order) as k_ras, organised so no CTA barrier couples elements:
 // each warp owns one element at a time in a grid-stride loop and synchronises with __syncwarp
 // only, so the gather, the FMA passes and the owner write of different warps overlap freely.
-// Warp-per-element RAS (FP32 FDM), the p >= 5 boxes (P = p + 3 >= 8). Line passes with a fixed
-// lane -> line map: lane = (u, w0) with u = lane % P, w0 = lane / P (G = 32 / P groups, P*G lanes
-// busy); the lane owns the lines w = w0 + G r (r < R = ceil(P / G)) of every pass, so all its
-// shared-memory addresses are one base register plus compile-time offsets. Per input value a
-// line pass costs one shared load and P scalar FFMA (FFMA issues at twice the flop rate of FFMA2
-// on this part: tools/peak_bench.cu); the factor rows are read as 16-byte broadcasts. The z pass
-// keeps its lines in registers through the forward transform, the inv_D scaling and the
-// backward transform. The next element's extended box (FP64, as stored) and factors arrive by
-// cp.async one element ahead.
-template <int P>
-struct LShape {
+// Gather and owner write walk the box / owned sites with x fastest across the lanes (coalesced
+// runs); the line passes stream the input lines from shared memory (accumulators in registers,
+// ~100 registers) so five CTAs of four warps fit per SM.
+template <int P, class T>
+struct WShape {
   static constexpr int P2 = P * P, P3 = P2 * P;
-  static constexpr int G = 32 / P;             // lane groups
-  static constexpr int R = (P + G - 1) / G;    // lines per lane per pass
-  static constexpr int SP = (P + 3) / 4 * 4;   // factor row stride (16-byte rows)
-  static constexpr int FAC = 3 * P * SP + 3 * SP;  // S_x, S_y, S_z rows, then lambda_x, _y, _z
-  static constexpr int WPC = 4;                // warps (elements in flight) per CTA
+  static constexpr int R = (P2 + 31) / 32;  // lines per lane
+  static constexpr int WPC = 4;             // warps (elements in flight) per CTA
   static constexpr int NT = 32 * WPC;
-  // per warp (floats): FP64 staging of the box, the FP32 box and tmp, the factors double-buffered
-  static constexpr int SPE = 2 * P3 + 2 * P3 + 2 * FAC;
-  static constexpr size_t smem() { return size_t(WPC) * SPE * sizeof(float); }
+  static constexpr int SPE = (2 * P3 + 3 * P2 + 3 * P + 3) / 4 * 4;  // box, tmp, S, L (16B multiple)
+  static constexpr size_t smem() { return size_t(WPC) * SPE * sizeof(T); }
 };
 
-// P entries of a 16-byte aligned factor row (broadcast loads)
-template <int P>
-__device__ __forceinline__ void load_row(const float* __restrict__ row, float (&s)[P]) {
-  constexpr int SP = LShape<P>::SP;
-  float v[SP];
-#pragma unroll
-  for (int q4 = 0; q4 < SP / 4; ++q4) {
-    const float4 t = *reinterpret_cast<const float4*>(row + 4 * q4);
-    v[4 * q4] = t.x;
-    v[4 * q4 + 1] = t.y;
-    v[4 * q4 + 2] = t.z;
-    v[4 * q4 + 3] = t.w;
-  }
-#pragma unroll
-  for (int o = 0; o < P; ++o) s[o] = v[o];
+template <int P, int AX>
+__device__ __forceinline__ int wline_base(int l) {
+  constexpr int P2 = P * P;
+  const int u = l % P, v = l / P;
+  return AX == 0 ? (v * P2 + u * P) : (AX == 1 ? (v * P2 + u) : (v * P + u));
 }
 
-// forward transform of the lane's R lines: y[r][o] = sum_a M(a, o) src[base + OFF r + STEP a]
-template <int P, int OFF, int STEP, class SrcT>
-__device__ __forceinline__ void lfwd(const SrcT* __restrict__ src, const float* __restrict__ M,
-                                     float (&y)[LShape<P>::R][P]) {
-  constexpr int R = LShape<P>::R, SP = LShape<P>::SP;
+template <int P, class T>
+__device__ __forceinline__ void load_pair(const T* M, T& s0, T& s1) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 v = *reinterpret_cast<const float2*>(M);
+    s0 = v.x;
+    s1 = v.y;
+  } else {
+    const double2 v = *reinterpret_cast<const double2*>(M);
+    s0 = v.x;
+    s1 = v.y;
+  }
+}
+
+// forward transform along AX: y[o] = sum_a M(a,o) x[a], x streamed from src, y in registers
+template <int P, class T, int AX>
+__device__ __forceinline__ void wfwd(const T* __restrict__ src, const T* __restrict__ M, const int (&base)[WShape<P, T>::R],
+                                     T (&y)[WShape<P, T>::R][P]) {
+  constexpr int R = WShape<P, T>::R;
+  constexpr int stride = AX == 0 ? 1 : (AX == 1 ? P : P * P);
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int o = 0; o < P; ++o) y[r][o] = 0.f;
-#pragma unroll
+    for (int o = 0; o < P; ++o) y[r][o] = T(0);
+#pragma unroll 2  // bounded: a full unroll hoists every S load and spills
   for (int a = 0; a < P; ++a) {
-    float xa[R];
+    T xa[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) xa[r] = float(src[OFF * r + STEP * a]);
-    float sr[P];
-    load_row<P>(M + a * SP, sr);
+    for (int r = 0; r < R; ++r) xa[r] = src[base[r] + a * stride];
+    if constexpr (P % 2 == 0 && sizeof(T) == 4 && SEMLAB_RASW_FFMA2) {
+      // packed FP32 (FFMA2): the (o, o+1) output pair shares x_a; same per-output order as below
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+      for (int o = 0; o < P; o += 2) {
+        const float2 s2 = *reinterpret_cast<const float2*>(M + a * P + o);
 #pragma unroll
-      for (int o = 0; o < P; ++o) y[r][o] = fmaf(sr[o], xa[r], y[r][o]);
-  }
-}
-
-// backward transform: out[r][a] = sum_o M(a, o) x[r][o], written to dst[OFF r + STEP a]
-template <int P, int OFF, int STEP>
-__device__ __forceinline__ void lbwd(const float (&x)[LShape<P>::R][P], const float* __restrict__ M,
-                                     const bool (&ok)[LShape<P>::R], float* __restrict__ dst) {
-  constexpr int R = LShape<P>::R, SP = LShape<P>::SP;
-#pragma unroll
-  for (int a = 0; a < P; ++a) {
-    float sr[P];
-    load_row<P>(M + a * SP, sr);
-    float acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      acc[r] = 0.f;
-#pragma unroll
-      for (int o = 0; o < P; ++o) acc[r] = fmaf(sr[o], x[r][o], acc[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (ok[r]) dst[OFF * r + STEP * a] = acc[r];
-  }
-}
-
-template <int P>
-__device__ __forceinline__ void lstore(const float (&y)[LShape<P>::R][P], const bool (&ok)[LShape<P>::R],
-                                       float* __restrict__ dst, int off, int step) {
-#pragma unroll
-  for (int r = 0; r < LShape<P>::R; ++r)
-    if (ok[r])
-#pragma unroll
-      for (int o = 0; o < P; ++o) dst[off * r + step * o] = y[r][o];
-}
-
-template <int P, int MODE>
-__global__ void __launch_bounds__(LShape<P>::NT, SEMLAB_RASW_MINB)
-    k_rasw(const Slab sl, const float* __restrict__ S, const float* __restrict__ L, const double* __restrict__ rin,
-           RasEpi epi) {
-  using W = LShape<P>;
-  constexpr int P2 = W::P2, P3 = W::P3, G = W::G, R = W::R, SP = W::SP, SPE = W::SPE, FAC = W::FAC;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* stage = reinterpret_cast<double*>(reinterpret_cast<float*>(smem_raw) + warp * SPE);
-  float* box = reinterpret_cast<float*>(stage + P3);
-  float* tmp = box + P3;
-  float* fac0 = tmp + P3;  // factors of even / odd iterations of this warp's element loop
-  const int nE = int(sl.elems());
-  const bool dir = sl.dirichlet != 0;
-  const int64_t NXY = sl.Nx * sl.Ny;
-  const int stride = gridDim.x * W::WPC;
-  // line map of this lane (idle lanes past P*G shadow lane 0 and never store)
-  const bool lane_on = lane < P * G;
-  const int u = lane_on ? lane % P : 0, w0 = lane_on ? lane / P : 0;
-  bool ok[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) ok[r] = lane_on && (w0 + G * r < P);
-
-  // Asynchronous loads of element e: the factor rows (padded to SP) and lambdas into fac, the
-  // extended box (FP64) into the staging buffer. Sites outside the box, and sites outside the
-  // element core in more than one direction (schwarz.cpp:255-265), are zero-filled by the copy
-  // itself (src-size 0). The box is gathered by z-columns: lane = (a, b) pair.
-  auto issue = [&](int e, float* fac) {
-    const int ex = e % sl.Ex, ey = (e / sl.Ex) % sl.Ey, ez = sl.ez0 + e / (sl.Ex * sl.Ey);
-    const Box1D X = box1d(ex, sl.Ex, sl.q, dir), Y = box1d(ey, sl.Ey, sl.q, dir), Z = box1d(ez, sl.Ez, sl.q, dir);
-    const float* se = S + int64_t(e) * 3 * P2;
-    for (int w = lane; w < 3 * P2; w += 32) {
-      const int d = w / P2, rem = w - d * P2, ra = rem / P, o = rem - ra * P;
-      cp_async4(fac + d * P * SP + ra * SP + o, se + w);
-    }
-    if (lane < 3 * P) {
-      const int d = lane / P;
-      cp_async4(fac + 3 * P * SP + d * SP + (lane - d * P), L + int64_t(e) * 3 * P + lane);
-    }
-    unsigned zin = 0, zcore = 0;  // c < Z.n; c < Z.n and not a z ghost
-#pragma unroll
-    for (int c = 0; c < P; ++c) {
-      zin |= unsigned(c < Z.n) << c;
-      zcore |= unsigned(c < Z.n && !ghost(Z, c)) << c;
-    }
-    const double* corner = rin + sl.lidx(X.lo, Y.lo, Z.lo);
-#pragma unroll 1
-    for (int l = lane; l < P2; l += 32) {
-      const int a = l % P, b = l / P;
-      const bool okab = a < X.n && b < Y.n;
-      const int gab = int(ghost(X, a)) + int(ghost(Y, b));
-      const unsigned m = !okab ? 0u : (gab == 0 ? zin : (gab == 1 ? zcore : 0u));
-      const double* col = corner + a + b * sl.Nx;
-#pragma unroll
-      for (int c = 0; c < P; ++c) {
-        const bool on = (m >> c) & 1u;
-        cp_async8(stage + c * P2 + l, on ? col + c * NXY : rin, on);
-      }
-    }
-    cp_async_commit();
-  };
-  int el = blockIdx.x * W::WPC + warp;
-  if (el < nE) issue(el, fac0);
-  for (int it = 0; el < nE; el += stride, ++it) {
-    const float* Sx = fac0 + (it & 1) * FAC;
-    const float* Sy = Sx + P * SP;
-    const float* Sz = Sy + P * SP;
-    const float* Lm = Sz + P * SP;  // lambda_x at Lm, lambda_y at Lm + SP, lambda_z at Lm + 2 SP
-    const int ex = el % sl.Ex, ey = (el / sl.Ex) % sl.Ey, ez = sl.ez0 + el / (sl.Ex * sl.Ey);
-    const Box1D X = box1d(ex, sl.Ex, sl.q, dir), Y = box1d(ey, sl.Ey, sl.q, dir), Z = box1d(ez, sl.Ez, sl.q, dir);
-    cp_async_wait_all();
-    __syncwarp();  // this element's box and factors are in shared memory for every lane
-    float y[R][P];
-    // x forward: lines (b, c) = (u, w): staged FP64 box -> tmp
-    lfwd<P, G * P2, 1>(stage + P * u + P2 * w0, Sx, y);
-    lstore<P>(y, ok, tmp + P * u + P2 * w0, G * P2, 1);
-    __syncwarp();  // the staging buffer and the other factor buffer are free: prefetch the next element
-    if (el + stride < nE) issue(el + stride, fac0 + ((it + 1) & 1) * FAC);
-    // y forward: lines (a, c) = (u, w): tmp -> box
-    lfwd<P, G * P2, P>(tmp + u + P2 * w0, Sy, y);
-    lstore<P>(y, ok, box + u + P2 * w0, G * P2, P);
-    __syncwarp();
-    // z: lines (a, b) = (u, w): forward, scale by inv_D = 1 / (lx_a + ly_b + lz_c), backward
-    lfwd<P, G * P, P2>(box + u + P * w0, Sz, y);
-    {
-      float lz[P];
-      load_row<P>(Lm + 2 * SP, lz);
-      const float lx = Lm[u];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const float lab = lx + Lm[SP + min(w0 + G * r, P - 1)];
-#pragma unroll
-        for (int o = 0; o < P; ++o) {
-          float inv;
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(lab + lz[o]));
-          y[r][o] *= inv;
+        for (int r = 0; r < R; ++r) {
+          const float2 acc = __ffma2_rn(s2, make_float2(xa[r], xa[r]), make_float2(y[r][o], y[r][o + 1]));
+          y[r][o] = acc.x;
+          y[r][o + 1] = acc.y;
         }
       }
+    } else if constexpr (P % 2 == 0) {
+#pragma unroll
+      for (int o = 0; o < P; o += 2) {
+        T s0, s1;
+        load_pair<P, T>(M + a * P + o, s0, s1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          y[r][o] = fma(s0, xa[r], y[r][o]);
+          y[r][o + 1] = fma(s1, xa[r], y[r][o + 1]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < P; ++o) {
+        const T sv = M[a * P + o];
+#pragma unroll
+        for (int r = 0; r < R; ++r) y[r][o] = fma(sv, xa[r], y[r][o]);
+      }
     }
-    lbwd<P, G * P, P2>(y, Sz, ok, tmp + u + P * w0);
+  }
+}
+
+// backward transform along AX: dst[a] = sum_o M(a,o) x[o], x in registers, rows written as formed
+template <int P, class T, int AX>
+__device__ __forceinline__ void wbwd(const T (&x)[WShape<P, T>::R][P], const T* __restrict__ M,
+                                     const int (&base)[WShape<P, T>::R], const bool (&ok)[WShape<P, T>::R],
+                                     T* __restrict__ dst) {
+  constexpr int R = WShape<P, T>::R;
+  constexpr int stride = AX == 0 ? 1 : (AX == 1 ? P : P * P);
+#pragma unroll 2
+  for (int a = 0; a < P; ++a) {
+    T acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = T(0);
+    if constexpr (P % 2 == 0 && sizeof(T) == 4 && SEMLAB_RASW_FFMA2) {
+      // packed FP32: even and odd o accumulate in the two halves, summed at the end
+      float2 a2[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a2[r] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int o = 0; o < P; o += 2) {
+        const float2 s2 = *reinterpret_cast<const float2*>(M + a * P + o);
+#pragma unroll
+        for (int r = 0; r < R; ++r) a2[r] = __ffma2_rn(s2, make_float2(x[r][o], x[r][o + 1]), a2[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = a2[r].x + a2[r].y;
+    } else if constexpr (P % 2 == 0) {
+#pragma unroll
+      for (int o = 0; o < P; o += 2) {
+        T s0, s1;
+        load_pair<P, T>(M + a * P + o, s0, s1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r] = fma(s0, x[r][o], acc[r]);
+          acc[r] = fma(s1, x[r][o + 1], acc[r]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < P; ++o) {
+        const T sv = M[a * P + o];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = fma(sv, x[r][o], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (ok[r]) dst[base[r] + a * stride] = acc[r];
+  }
+}
+
+template <int P, class T, int AX>
+__device__ __forceinline__ void wbases(int lane, int (&base)[WShape<P, T>::R], bool (&ok)[WShape<P, T>::R]) {
+#pragma unroll
+  for (int r = 0; r < WShape<P, T>::R; ++r) {
+    const int l = lane + 32 * r;
+    ok[r] = l < P * P;
+    base[r] = ok[r] ? wline_base<P, AX>(l) : 0;  // idle lines read a valid address, never write
+  }
+}
+
+#ifndef SEMLAB_RASW_PF
+#define SEMLAB_RASW_PF 0  // L2 prefetch of the next element's box rows and factors
+#endif
+
+template <int P, class T, int MODE>
+__global__ void __launch_bounds__(WShape<P, T>::NT, sizeof(T) == 4 ? SEMLAB_RASW_MINB : 2)
+    k_rasw(const Slab sl, const T* __restrict__ S, const T* __restrict__ L, const double* __restrict__ rin,
+           RasEpi epi) {
+  using W = WShape<P, T>;
+  constexpr int P2 = W::P2, P3 = W::P3, R = W::R, SPE = W::SPE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* box = reinterpret_cast<T*>(smem_raw) + warp * SPE;
+  T* tmp = box + P3;
+  T* Se = tmp + P3;
+  T* Le = Se + 3 * P2;
+  const int nE = int(sl.elems());
+  const bool dir = sl.dirichlet != 0;
+  for (int el = blockIdx.x * W::WPC + warp; el < nE; el += gridDim.x * W::WPC) {
+    const int ex = el % sl.Ex, ey = (el / sl.Ex) % sl.Ey, ez = sl.ez0 + el / (sl.Ex * sl.Ey);
+    const Box1D X = box1d(ex, sl.Ex, sl.q, dir), Y = box1d(ey, sl.Ey, sl.q, dir), Z = box1d(ez, sl.Ez, sl.q, dir);
+#if SEMLAB_RASW_PF
+    {  // the next element's extended-box rows (and factors) -> L2 while this element is solved
+      const int en = el + gridDim.x * W::WPC;
+      if (en < nE) {
+        const int nx = en % sl.Ex, ny = (en / sl.Ex) % sl.Ey, nz = sl.ez0 + en / (sl.Ex * sl.Ey);
+        const Box1D NX = box1d(nx, sl.Ex, sl.q, dir), NY = box1d(ny, sl.Ey, sl.q, dir), NZ = box1d(nz, sl.Ez, sl.q, dir);
+        const double* nc = rin + sl.lidx(NX.lo, NY.lo, NZ.lo);
+        const int64_t NXY = sl.Nx * sl.Ny;
+        for (int rw = lane; rw < NY.n * NZ.n; rw += 32) {
+          const double* p = nc + (rw % NY.n) * sl.Nx + (rw / NY.n) * NXY;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p + NX.n - 1));
+        }
+        if (lane < (3 * P2 * int(sizeof(T)) + 127) / 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(S + int64_t(en) * 3 * P2) + lane * 128));
+      }
+    }
+#endif
+    __syncwarp();  // the previous element's owner write has finished reading tmp
+    {  // factors: S (3 P^2) and lambda (3 P), all loads issued before the stores
+      constexpr int NF = 3 * P2 + 3 * P, IT = (NF + 31) / 32;
+      T v[IT];
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int w = lane + 32 * it;
+        v[it] = w < 3 * P2 ? __ldg(S + int64_t(el) * 3 * P2 + w)
+                           : (w < NF ? __ldg(L + int64_t(el) * 3 * P + (w - 3 * P2)) : T(0));
+      }
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int w = lane + 32 * it;
+        if (w < NF) Se[w] = v[it];
+      }
+    }
+    {  // gather the extended box by z-columns: lane = (a, b) pair, loop over c, so the x/y
+       // validity and the column address are fixed per pair and the z test is a bit mask; sites
+       // outside the core in more than one direction (and outside a smaller boundary box) are zero
+       // (schwarz.cpp:255-265)
+      unsigned zin = 0, zcore = 0;  // c < Z.n; c < Z.n and not a z ghost
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        zin |= unsigned(c < Z.n) << c;
+        zcore |= unsigned(c < Z.n && !ghost(Z, c)) << c;
+      }
+      const int64_t NXY = sl.Nx * sl.Ny;
+      const double* corner = rin + sl.lidx(X.lo, Y.lo, Z.lo);
+#pragma unroll kGatherUnroll
+      for (int r = 0; r < R; ++r) {
+        const int l = min(lane + 32 * r, P2 - 1);  // lanes past the last pair redo it (same values)
+        const int a = l % P, b = l / P;
+        const bool okab = a < X.n && b < Y.n;
+        const int gab = int(ghost(X, a)) + int(ghost(Y, b));
+        const unsigned m = !okab ? 0u : (gab == 0 ? zin : (gab == 1 ? zcore : 0u));
+        const double* col = corner + a + b * sl.Nx;
+        double v[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) v[c] = __ldg((m >> c) & 1u ? col + c * NXY : rin);
+#pragma unroll
+        for (int c = 0; c < P; ++c) box[c * P2 + l] = (m >> c) & 1u ? T(v[c]) : T(0);
+      }
+    }
     __syncwarp();
-    // y backward: lines (a, c): tmp -> box
+    int base[R];
+    bool okl[R];
+    T y[R][P];
+    wbases<P, T, 0>(lane, base, okl);
+    wfwd<P, T, 0>(box, Se + 0 * P2, base, y);  // x forward: box -> tmp
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (okl[r])
+#pragma unroll
+        for (int o = 0; o < P; ++o) tmp[base[r] + o] = y[r][o];
+    __syncwarp();
+    wbases<P, T, 1>(lane, base, okl);
+    wfwd<P, T, 1>(tmp, Se + 1 * P2, base, y);  // y forward: tmp -> box
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (okl[r])
+#pragma unroll
+        for (int o = 0; o < P; ++o) box[base[r] + o * P] = y[r][o];
+    __syncwarp();
+    wbases<P, T, 2>(lane, base, okl);
+    wfwd<P, T, 2>(box, Se + 2 * P2, base, y);  // z forward, scale by inv_D, z backward: box -> tmp
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int l = lane + 32 * r;
+      const int a = l % P, b = (l / P) % P;
+      const T lab = Le[0 * P + a] + Le[1 * P + b];
+#pragma unroll
+      for (int c = 0; c < P; ++c) y[r][c] = y[r][c] * rcp(lab + Le[2 * P + c]);
+    }
+    wbwd<P, T, 2>(y, Se + 2 * P2, base, okl, tmp);
+    __syncwarp();
+    wbases<P, T, 1>(lane, base, okl);  // y backward: tmp -> box
     {
-      const float* src = tmp + u + P2 * w0;
+      constexpr int stride = P;
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int o = 0; o < P; ++o) y[r][o] = src[G * P2 * r + P * o];
+        for (int m = 0; m < P; ++m) y[r][m] = tmp[base[r] + m * stride];
     }
-    lbwd<P, G * P2, P>(y, Sy, ok, box + u + P2 * w0);
+    wbwd<P, T, 1>(y, Se + 1 * P2, base, okl, box);
     __syncwarp();
-    // x backward: lines (b, c): box -> tmp
-    {
-      const float* src = box + P * u + P2 * w0;
+    wbases<P, T, 0>(lane, base, okl);  // x backward: box -> tmp
 #pragma unroll
-      for (int r = 0; r < R; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int o = 0; o < P; ++o) y[r][o] = src[G * P2 * r + o];
-    }
-    lbwd<P, G * P2, 1>(y, Sx, ok, tmp + P * u + P2 * w0);
+      for (int m = 0; m < P; ++m) y[r][m] = box[base[r] + m];
+    wbwd<P, T, 0>(y, Se + 0 * P2, base, okl, tmp);
     __syncwarp();
     // owner write by z-columns: lane = (a, b) over the owned face (QA x QA, power of two so the
     // split is a shift), U consecutive c per round with every vector load issued before the stores
     const int na = X.own_hi - X.own_lo + 1, nb = Y.own_hi - Y.own_lo + 1, nc = Z.own_hi - Z.own_lo + 1;
     constexpr int QA = (P - 2) <= 4 ? 4 : ((P - 2) <= 8 ? 8 : 16);
     constexpr int U = SEMLAB_RASW_OWNER_U;
+    const int64_t NXY = sl.Nx * sl.Ny;
 #pragma unroll 1
     for (int pr = lane; pr < QA * QA; pr += 32) {
       const int oa = pr % QA, ob = pr / QA;
       if (oa >= na || ob >= nb) continue;
       const int aa = X.own_lo + oa, bb = Y.own_lo + ob;
       const int64_t g0 = sl.lidx(X.lo + aa, Y.lo + bb, Z.lo + Z.own_lo);
-      const float* zt = tmp + Z.own_lo * P2 + bb * P + aa;
+      const T* zt = tmp + Z.own_lo * P2 + bb * P + aa;
 #pragma unroll 1
       for (int c0 = 0; c0 < nc; c0 += U) {
         int64_t g[U];
-        bool okc[U];
+        bool ok[U];
         double z[U];
 #pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-          const int c = c0 + uu;
-          okc[uu] = c < nc;
-          g[uu] = okc[uu] ? g0 + c * NXY : g0;
-          z[uu] = okc[uu] ? double(zt[c * P2]) : 0.0;
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u;
+          ok[u] = c < nc;
+          g[u] = ok[u] ? g0 + c * NXY : g0;
+          z[u] = ok[u] ? double(zt[c * P2]) : 0.0;
         }
         if (MODE == 0) {
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu)
-            if (okc[uu]) epi.out[g[uu]] = z[uu];
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) epi.out[g[u]] = z[u];
         } else if (MODE == 1) {  // Chebyshev init: r = S t, d = r / theta  (chebyshev.cpp:82-84)
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu)
-            if (okc[uu]) {
-              epi.r[g[uu]] = z[uu];
-              epi.d[g[uu]] = z[uu] * epi.c2;  // c2 = 1 / theta
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) {
+              epi.r[g[u]] = z[u];
+              epi.d[g[u]] = z[u] * epi.c2;  // c2 = 1 / theta (FP64 division per node was 11% of the stalls)
             }
         } else {  // Chebyshev step: x += d; r -= S A d; d = c1 d + c2 r  (chebyshev.cpp:86-92)
           double dv[U], rv[U], xv[U];
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu) {
-            dv[uu] = epi.d[g[uu]];
-            rv[uu] = epi.r[g[uu]];
-            xv[uu] = epi.x[g[uu]];
+          for (int u = 0; u < U; ++u) {
+            dv[u] = epi.d[g[u]];
+            rv[u] = epi.r[g[u]];
+            xv[u] = epi.x[g[u]];
           }
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu)
-            if (okc[uu]) {
-              const double x1 = xv[uu] + dv[uu];
-              const double rg = rv[uu] - z[uu];
-              const double dn = epi.c1 * dv[uu] + epi.c2 * rg;
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) {
+              const double x1 = xv[u] + dv[u];
+              const double rg = rv[u] - z[u];
+              const double dn = epi.c1 * dv[u] + epi.c2 * rg;
               if (MODE == 3) {  // last step: the final x += d fused, r and d are dead afterwards
-                epi.x[g[uu]] = x1 + dn;
+                epi.x[g[u]] = x1 + dn;
               } else {
-                epi.x[g[uu]] = x1;
-                epi.r[g[uu]] = rg;
-                epi.d[g[uu]] = dn;
+                epi.x[g[u]] = x1;
+                epi.r[g[u]] = rg;
+                epi.d[g[u]] = dn;
               }
             }
         }
@@ -746,23 +808,21 @@ template <class T>
 struct Launch {
   // warp-per-element RAS for the large boxes (SEMLAB_RAS_WARP=0 selects the CTA-per-group kernel)
   template <int P, int MODE>
-  static void rasw(const Slab& sl, const float* S, const float* L, const double* r, const RasEpi& e, cudaStream_t s) {
-    using W = LShape<P>;
-    auto kern = k_rasw<P, MODE>;
+  static void rasw(const Slab& sl, const T* S, const T* L, const double* r, const RasEpi& e, cudaStream_t s) {
+    using W = WShape<P, T>;
+    auto kern = k_rasw<P, T, MODE>;
     const int nctas = resident_ctas(kern, W::NT, W::smem());
     const int64_t need = (sl.elems() + W::WPC - 1) / W::WPC;
     kern<<<capped_grid(std::min<int64_t>(need, nctas)), W::NT, W::smem(), s>>>(sl, S, L, r, e);
   }
   template <int P>
   static void ras(const Slab& sl, const T* S, const T* L, const double* r, int mode, const RasEpi& e, cudaStream_t s) {
-    if constexpr (sizeof(T) == 4 && P >= SEMLAB_RASW_MINP) {
-      if (ras_warp() && sl.elems() < (int64_t(1) << 31)) {
-        if (mode == 0) rasw<P, 0>(sl, S, L, r, e, s);
-        else if (mode == 1) rasw<P, 1>(sl, S, L, r, e, s);
-        else if (mode == 2) rasw<P, 2>(sl, S, L, r, e, s);
-        else rasw<P, 3>(sl, S, L, r, e, s);
-        return;
-      }
+    if (sizeof(T) == 4 && P >= SEMLAB_RASW_MINP && ras_warp() && sl.elems() < (int64_t(1) << 31)) {
+      if (mode == 0) rasw<P, 0>(sl, S, L, r, e, s);
+      else if (mode == 1) rasw<P, 1>(sl, S, L, r, e, s);
+      else if (mode == 2) rasw<P, 2>(sl, S, L, r, e, s);
+      else rasw<P, 3>(sl, S, L, r, e, s);
+      return;
     }
     using Sh = Shape<P, T>;
     const int grid = int((sl.elems() + Sh::EPC - 1) / Sh::EPC);

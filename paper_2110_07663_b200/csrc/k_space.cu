@@ -953,52 +953,88 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
 }
 
 // Face nodes of the slab: (a) planes z % q == 0, (b) z % q != 0 with y % q == 0, (c) z, y % q != 0
-// with x % q == 0. Each sums its contributors' face-buffer entries in ascending element id.
+// with x % q == 0 — consecutive threads walk x in every family. Each node sums its contributors'
+// face-buffer entries in ascending element id: the (lower, upper) candidates of z, then y, then
+// x, all eight loads predicated and issued together.
+struct Cand2 {  // the <= 2 elements along one axis containing a lattice coordinate (lower first)
+  int e0, l0, e1, l1;
+  bool v0, v1;
+};
+__device__ __forceinline__ Cand2 cand2(int c, int q, int lo_e, int hi_e) {
+  Cand2 r;
+  const int e = c / q, l = c - e * q;
+  if (l == 0) {  // on an element boundary: lower element (local q), upper element (local 0)
+    r.e0 = e - 1;
+    r.l0 = q;
+    r.v0 = e - 1 >= lo_e;
+    r.e1 = e;
+    r.l1 = 0;
+    r.v1 = e < hi_e;
+  } else {
+    r.e0 = e;
+    r.l0 = l;
+    r.v0 = true;
+    r.e1 = e;
+    r.l1 = l;
+    r.v1 = false;
+  }
+  return r;
+}
+
+// One face lattice node (x, y, z): sum its contributors' face-buffer entries in ascending element
+// id — the (lower, upper) candidates of z, then y, then x, all eight loads predicated and issued
+// together — apply the Dirichlet mask and the epilogue.
 template <class EpiT>
-__global__ void __launch_bounds__(256) k_face_epi7(const Slab sl, const double* __restrict__ fb, const EpiT epi) {
+__device__ __forceinline__ void face_node7(const Slab& sl, const double* __restrict__ fb, const EpiT& epi, int x,
+                                           int y, int z) {
   using namespace axw;
   constexpr int q = 7;
-  const int64_t Nx = sl.Nx, Ny = sl.Ny;
-  const int nzl = sl.ez1 - sl.ez0;               // element layers on this rank
-  const int64_t na = int64_t(nzl + 1) * Nx * Ny;  // (a)
-  const int64_t nb = int64_t(nzl) * (q - 1) * (sl.Ey + 1) * Nx;          // (b)
-  const int64_t nc = int64_t(nzl) * (q - 1) * (int64_t(sl.Ey) * (q - 1)) * (sl.Ex + 1);  // (c)
-  const int64_t total = na + nb + nc;
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-    int64_t x, y, z;
-    if (t < na) {
-      x = t % Nx;
-      y = (t / Nx) % Ny;
-      z = int64_t(sl.ez0) * q + (t / (Nx * Ny)) * q;
-    } else if (t < na + nb) {
-      const int64_t s = t - na;
-      x = s % Nx;
-      y = ((s / Nx) % (sl.Ey + 1)) * q;
-      const int64_t zz = s / (Nx * (sl.Ey + 1));  // 0 .. nzl (q-1) - 1
-      z = int64_t(sl.ez0) * q + (zz / (q - 1)) * q + 1 + zz % (q - 1);
-    } else {
-      const int64_t s = t - na - nb;
-      x = (s % (sl.Ex + 1)) * q;
-      const int64_t yy = (s / (sl.Ex + 1)) % (int64_t(sl.Ey) * (q - 1));
-      y = (yy / (q - 1)) * q + 1 + yy % (q - 1);
-      const int64_t zz = s / ((sl.Ex + 1) * (int64_t(sl.Ey) * (q - 1)));
-      z = int64_t(sl.ez0) * q + (zz / (q - 1)) * q + 1 + zz % (q - 1);
-    }
-    const int64_t g = sl.lidx(x, y, z);
-    if (sl.masked(x, y, z)) {
-      epi(g, 0.0);
-      continue;
-    }
-    const Cands cx = cands(x, q, sl.Ex, 0, sl.Ex), cy = cands(y, q, sl.Ey, 0, sl.Ey);
-    const Cands cz = cands(z, q, sl.Ez, sl.ez0, sl.ez1);
-    double acc = 0.0;
-    for (int c = 0; c < cz.n; ++c)
-      for (int b = 0; b < cy.n; ++b)
-        for (int a = 0; a < cx.n; ++a) {
-          const int64_t el = cx.e[a] + int64_t(sl.Ex) * (cy.e[b] + int64_t(sl.Ey) * (cz.e[c] - sl.ez0));
-          acc += fb[el * FACE + face_idx(cx.loc[a], cy.loc[b], cz.loc[c])];
-        }
-    epi(g, acc);
+  const int64_t g = sl.lidx(x, y, z);
+  if (sl.masked(x, y, z)) {
+    epi(g, 0.0);
+    return;
+  }
+  const Cand2 cx = cand2(x, q, 0, sl.Ex), cy = cand2(y, q, 0, sl.Ey), cz = cand2(z, q, sl.ez0, sl.ez1);
+  double v[8];
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const bool on = (c ? cz.v1 : cz.v0) && (b ? cy.v1 : cy.v0) && (a ? cx.v1 : cx.v0);
+        const int ez = (c ? cz.e1 : cz.e0) - sl.ez0, ey = b ? cy.e1 : cy.e0, ex = a ? cx.e1 : cx.e0;
+        const int el = ex + sl.Ex * (ey + sl.Ey * ez);
+        const double* p = fb + size_t(el) * FACE + face_idx(a ? cx.l1 : cx.l0, b ? cy.l1 : cy.l0, c ? cz.l1 : cz.l0);
+        v[c * 4 + b * 2 + a] = on ? __ldcs(p) : 0.0;
+      }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc += v[k];  // ascending element id; absent contributors add +0.0
+  epi(g, acc);
+}
+
+// The slab's face nodes in three launches of 2-D grids (x along the threads, no divisions):
+//   FAM 0: planes z = q k (all x, y)        grid (., Ny, nzl + 1)
+//   FAM 1: z % q != 0, y = q j (all x)      grid (., Ey + 1, nzl (q-1))
+//   FAM 2: z, y % q != 0, x = q i           grid (., Ey, nzl (q-1)), threads over (i, y in the row)
+template <int FAM, class EpiT>
+__global__ void __launch_bounds__(128) k_face_epi7(const Slab sl, const double* __restrict__ fb, const EpiT epi) {
+  constexpr int q = 7;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int zb = sl.ez0 * q;
+  if (FAM == 0) {
+    if (t >= sl.Nx) return;
+    face_node7(sl, fb, epi, t, int(blockIdx.y), zb + int(blockIdx.z) * q);
+  } else if (FAM == 1) {
+    if (t >= sl.Nx) return;
+    const int zz = int(blockIdx.z);
+    face_node7(sl, fb, epi, t, int(blockIdx.y) * q, zb + (zz / (q - 1)) * q + 1 + zz % (q - 1));
+  } else {  // threads over (x-plane i, y inside the element row): t = 6 i + (y - q ey - 1)
+    const int i = t / (q - 1), yi = t - i * (q - 1);
+    if (i > sl.Ex) return;
+    const int zz = int(blockIdx.z);
+    face_node7(sl, fb, epi, i * q, int(blockIdx.y) * q + 1 + yi, zb + (zz / (q - 1)) * q + 1 + zz % (q - 1));
   }
 }
 
@@ -1017,11 +1053,12 @@ int64_t axw_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
   const int grid = capped_grid(std::min<int64_t>(nctas, (nE + W - 1) / W));
   kern<<<grid, 32 * W, smem, s>>>(sl, dmat<8>(sl.q), u, geom, sy.dep, epi);
   SB_LAUNCH_CHECK();
-  const int64_t nzl = sl.ez1 - sl.ez0;
-  const int64_t faces = (nzl + 1) * sl.Nx * sl.Ny + nzl * 6 * (sl.Ey + 1) * sl.Nx + nzl * 6 * (sl.Ey * 6) * (sl.Ex + 1);
-  k_face_epi7<<<capped_grid(std::min<int64_t>((faces + 255) / 256, 148 * 16)), 256, 0, s>>>(sl, sy.dep, epi);
+  const unsigned nzl = unsigned(sl.ez1 - sl.ez0), bx = unsigned((sl.Nx + 127) / 128);
+  k_face_epi7<0><<<dim3(bx, unsigned(sl.Ny), nzl + 1), 128, 0, s>>>(sl, sy.dep, epi);
+  k_face_epi7<1><<<dim3(bx, unsigned(sl.Ey + 1), nzl * 6), 128, 0, s>>>(sl, sy.dep, epi);
+  k_face_epi7<2><<<dim3(unsigned(((sl.Ex + 1) * 6 + 127) / 128), unsigned(sl.Ey), nzl * 6), 128, 0, s>>>(sl, sy.dep, epi);
   SB_LAUNCH_CHECK();
-  return 2;
+  return 4;
 }
 
 bool ax_dmma() {  // SEMLAB_AX_DMMA=0 selects the FP64-FMA persistent kernel (A/B measurement)

@@ -35,7 +35,7 @@ def rel(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
 
 
-@pytest.mark.parametrize("eps,E,p", [(0.3, 6, 7), (1.0, 5, 7), (0.3, 4, 8), (0.3, 6, 3)])
+@pytest.mark.parametrize("eps,E,p", [(0.3, 6, 7), (1.0, 8, 7), (0.3, 4, 8), (0.3, 6, 3)])
 def test_ax_grid_cap_bitwise(ctx, eps, E, p):
     from paper_2110_07663_b200 import semlab as S
     sp = S.SemSpace(S.generate_kershaw(eps, E, ctx), p)
