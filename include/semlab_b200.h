@@ -58,6 +58,10 @@ typedef struct semlab_pmg_s* semlab_pmg;         /* pMG hierarchy (pmg.cpp is MI
 #define SEMLAB_SMOOTHER_JACOBI 0
 #define SEMLAB_SMOOTHER_RAS 1
 #define SEMLAB_SMOOTHER_ASM 2
+#define SEMLAB_SMOOTHER_RAS_PLAIN 3 /* un-accelerated RAS: x = S b pre, x += S (b - A x) post  */
+#define SEMLAB_SMOOTHER_ASM_PLAIN 4 /* un-accelerated ASM (MgLevel smoother kinds) */
+#define SEMLAB_CYCLE_STANDARD 0 /* Alg. 1: pre-smooth, coarse correction, post-smooth          */
+#define SEMLAB_CYCLE_ADDITIVE 1 /* additive V-cycle, no post-smoothing (PAPER §2.2.2) */
 #define SEMLAB_COARSE_DIRECT 0 /* exact solve of the p=1 system (SPEC.md:341-344 default) */
 #define SEMLAB_COARSE_AMG 1    /* one AmgHierarchy V-cycle (amg.hpp:34-37)   */
 
@@ -194,6 +198,19 @@ int semlab_cheby_destroy(semlab_cheby c);
 int semlab_cheby_smooth(semlab_cheby c, const double* d_b, double* d_x);
 
 /* ---- p-multigrid (RESTATED: pmg.cpp missing, Alg. 1) ------------ */
+typedef struct { /* hierarchy options */
+  int smoother;           /* SEMLAB_SMOOTHER_* */
+  int cheb_order;         /* Chebyshev order eta (Chebyshev smoothers) */
+  double lambda_min_mult; /* Chebyshev bounds (0.1, 1.1) lambda~ */
+  double lambda_max_mult;
+  int precision;          /* Schwarz FDM precision: 32 (paper) or 64 */
+  int coarse;             /* SEMLAB_COARSE_* */
+  int bc;                 /* SEMLAB_BC_*: Neumann builds every level in Neumann mode and solves the
+                             singular coarse problem on the zero-mean subspace (direct coarse only) */
+  int cycle;              /* SEMLAB_CYCLE_* */
+} semlab_pmg_options;
+int semlab_pmg_create_ex(semlab_mesh mesh, int nlevels, const int* orders, const semlab_pmg_options* opts,
+                         semlab_pmg* out);
 /* orders: strictly decreasing schedule ending at 1, e.g. {7,3,1}. smoother: SEMLAB_SMOOTHER_*;
    precision applies to Schwarz smoothers (32 or 64). coarse: SEMLAB_COARSE_*. */
 int semlab_pmg_create(semlab_mesh mesh, int nlevels, const int* orders, int smoother,

@@ -386,6 +386,41 @@ int ref_case_solve(void* h, int krylov, int restart, double tol, int max_iters, 
   });
 }
 
+// V-cycle with the extended pMG options (plain smoothers, additive cycle, Neumann levels): z = M b.
+int ref_vcycle_ex(double eps, int E, const int* orders, int nlev, const char* smoother, const char* coarse, int eta,
+                  int neumann, int additive, const double* b, double* z) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, orders[0]);
+    Pmg pmg(m, orders_of(orders, nlev), smoother, eta, 0.1, 1.1, coarse,
+            neumann ? BcMode::Neumann : BcMode::Dirichlet, additive != 0);
+    const Index n = pmg.spaces[0]->n();
+    FieldVector bv = Eigen::Map<const Eigen::MatrixXd>(b, n, 1);
+    FieldVector zv = pmg.vcycle(bv);
+    std::memcpy(z, zv.data(), sizeof(double) * size_t(n));
+  });
+}
+
+// GMRES(20) to tol with that preconditioner on b (caller's vector), x0 = 0.
+int ref_solve_ex(double eps, int E, const int* orders, int nlev, const char* smoother, const char* coarse, int eta,
+                 int neumann, int additive, const double* b, double tol, double* x, int* iters, double* rel_res) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, orders[0]);
+    Pmg pmg(m, orders_of(orders, nlev), smoother, eta, 0.1, 1.1, coarse,
+            neumann ? BcMode::Neumann : BcMode::Dirichlet, additive != 0);
+    const SemSpace* s0 = pmg.spaces[0].get();
+    LinOp A = [s0](const FieldVector& in, FieldVector& out) { out = s0->apply_A(in); };
+    LinOp M = pmg.as_linop();
+    FieldVector bv = Eigen::Map<const Eigen::MatrixXd>(b, s0->n(), 1);
+    FieldVector xv = FieldVector::Zero(s0->n());
+    GmresConfig cfg;
+    cfg.tol = tol;
+    const GmresStats st = gmres_solve(A, M, bv, xv, cfg);
+    std::memcpy(x, xv.data(), sizeof(double) * size_t(s0->n()));
+    *iters = st.iterations;
+    *rel_res = st.rel_residual;
+  });
+}
+
 // AMG hierarchy of the p=1 coarse problem (CoarseSolve "amg"): level sizes and the level-0
 // aggregate of every free dof (tests compare the product's hierarchy against it).
 int ref_amg_info(double eps, int E, int* nlev, int64_t* sizes, int cap, int* agg0) {

@@ -131,7 +131,13 @@ CoarseSolve::CoarseSolve(const SemSpace& s, const std::string& mode) : sp(&s), m
   A_.resize(nf, nf);
   A_.setFromTriplets(trip.begin(), trip.end());
   if (mode_ == "direct") {
-    ldlt_.compute(Eigen::MatrixXd(A_));
+    Eigen::MatrixXd Ad(A_);
+    if (s.bc() == BcMode::Neumann) {  // constants span the nullspace: A + 1 1^T / n is SPD
+      const double c = 1.0 / double(nf);
+      for (Index j = 0; j < nf; ++j)
+        for (Index i = 0; i < nf; ++i) Ad(i, j) += c;
+    }
+    ldlt_.compute(Ad);
     if (ldlt_.info() != Eigen::Success) throw std::runtime_error("coarse: factorization failed");
   } else {
     amg_ = std::make_unique<AmgHierarchy>(AmgHierarchy::build(A_));
@@ -142,19 +148,25 @@ FieldVector CoarseSolve::solve(const FieldVector& r) const {
   const Index nf = Index(free_.size());
   FieldVector rf(nf), zf;
   for (Index t = 0; t < nf; ++t) rf[t] = r[free_[size_t(t)]];
+  const bool neu = sp->bc() == BcMode::Neumann;
+  if (neu) rf.array() -= rf.mean();  // project onto the zero-mean range, solve, project back
   if (mode_ == "direct")
     zf = ldlt_.solve(rf);
   else
     amg_->vcycle(rf, zf);
+  if (neu) zf.array() -= zf.mean();
   FieldVector z = FieldVector::Zero(sp->n());
   for (Index t = 0; t < nf; ++t) z[free_[size_t(t)]] = zf[t];
   return z;
 }
 
 // ---------------------------------------------------------------- pMG (Alg. 1)
-Pmg::Pmg(const HexMesh& mesh, const std::vector<int>& orders, const std::string& smoother, int eta, double lmin,
-         double lmax, const std::string& coarse) {
-  for (int q : orders) spaces.push_back(std::make_unique<SemSpace>(mesh, q));
+Pmg::Pmg(const HexMesh& mesh, const std::vector<int>& orders, const std::string& smoother_kind, int eta, double lmin,
+         double lmax, const std::string& coarse, BcMode bc, bool additive) {
+  plain_ = smoother_kind == "ras_plain" || smoother_kind == "asm_plain";
+  additive_ = additive;
+  const std::string smoother = plain_ ? smoother_kind.substr(0, 3) : smoother_kind;
+  for (int q : orders) spaces.push_back(std::make_unique<SemSpace>(mesh, q, bc));
   for (size_t l = 0; l + 1 < orders.size(); ++l) {
     const SemSpace& s = *spaces[l];
     Level L;
@@ -166,25 +178,55 @@ Pmg::Pmg(const HexMesh& mesh, const std::vector<int>& orders, const std::string&
       L.sch = std::make_unique<SchwarzSmoother>(s, smoother == "ras" ? SchwarzMode::Ras : SchwarzMode::Asm);
       L.S = L.sch->as_linop();
     }
-    L.lam = estimate_lambda_max(L.S, L.A, s.n(), 10, 0).value;
-    L.cheb = std::make_unique<ChebyshevSmoother>(L.S, L.A, ChebyParams{eta, lmin, lmax, L.lam});
+    if (!plain_) {
+      L.lam = estimate_lambda_max(L.S, L.A, s.n(), 10, 0).value;
+      L.cheb = std::make_unique<ChebyshevSmoother>(L.S, L.A, ChebyParams{eta, lmin, lmax, L.lam});
+    }
     levels.push_back(std::move(L));
     transfers.push_back(std::make_unique<Transfer>(s, *spaces[l + 1]));
   }
   coarse_ = std::make_unique<CoarseSolve>(*spaces.back(), coarse);
 }
 
+// one smoothing step: Chebyshev(eta) from x (x = 0 when null), or the plain smoother:
+// x = S b from zero, else x + S (b - A x)
+FieldVector Pmg::smooth(size_t l, const FieldVector& b, const FieldVector* x0) const {
+  const Level& L = levels[l];
+  FieldVector x = x0 ? *x0 : FieldVector::Zero(b.size());
+  if (!plain_) {
+    L.cheb->smooth(b, x);
+    return x;
+  }
+  FieldVector t(b.size()), z(b.size());
+  if (!x0) {
+    L.S(b, z);
+    return z;
+  }
+  L.A(x, t);
+  t = b - t;
+  L.S(t, z);
+  x += z;
+  return x;
+}
+
 FieldVector Pmg::cycle(size_t l, const FieldVector& b) const {
   if (l == levels.size()) return coarse_->solve(b);
   const Level& L = levels[l];
-  FieldVector x = FieldVector::Zero(b.size());
-  L.cheb->smooth(b, x);
+  FieldVector x = smooth(l, b, nullptr);
   FieldVector r(b.size());
   L.A(x, r);
   r = b - r;
   FieldVector ec = cycle(l + 1, transfers[l]->restrict_(r));
   x += transfers[l]->prolong(ec);
-  L.cheb->smooth(b, x);
+  return smooth(l, b, &x);
+}
+
+// additive V-cycle: smooth every level's restricted right-hand side from zero,
+// solve the coarsest, sum the prolongated corrections; no residual re-evaluation, no post-smoothing
+FieldVector Pmg::cycle_additive(size_t l, const FieldVector& b) const {
+  if (l == levels.size()) return coarse_->solve(b);
+  FieldVector x = smooth(l, b, nullptr);
+  x += transfers[l]->prolong(cycle_additive(l + 1, transfers[l]->restrict_(b)));
   return x;
 }
 

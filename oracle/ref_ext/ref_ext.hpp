@@ -29,7 +29,7 @@ struct Transfer {
 
 class CoarseSolve {
  public:
-  CoarseSolve(const semlab::SemSpace& s, const std::string& mode);
+  CoarseSolve(const semlab::SemSpace& s, const std::string& mode);  // Neumann space: zero-mean solve
   semlab::FieldVector solve(const semlab::FieldVector& r) const;
   const semlab::AmgHierarchy* amg() const { return amg_.get(); }
 
@@ -44,9 +44,11 @@ class CoarseSolve {
 
 class Pmg {
  public:
+  // smoother: "jacobi" | "ras" | "asm" (Chebyshev-accelerated) | "ras_plain" | "asm_plain";
+  // additive: the additive V-cycle without post-smoothing
   Pmg(const semlab::HexMesh& mesh, const std::vector<int>& orders, const std::string& smoother, int eta, double lmin,
-      double lmax, const std::string& coarse);
-  semlab::FieldVector vcycle(const semlab::FieldVector& b) const { return cycle(0, b); }
+      double lmax, const std::string& coarse, semlab::BcMode bc = semlab::BcMode::Dirichlet, bool additive = false);
+  semlab::FieldVector vcycle(const semlab::FieldVector& b) const { return additive_ ? cycle_additive(0, b) : cycle(0, b); }
   semlab::LinOp as_linop() const;
   struct Level {
     semlab::LinOp A, S;
@@ -60,6 +62,9 @@ class Pmg {
 
  private:
   semlab::FieldVector cycle(size_t l, const semlab::FieldVector& b) const;
+  semlab::FieldVector cycle_additive(size_t l, const semlab::FieldVector& b) const;
+  semlab::FieldVector smooth(size_t l, const semlab::FieldVector& b, const semlab::FieldVector* x) const;
+  bool plain_ = false, additive_ = false;
   std::unique_ptr<CoarseSolve> coarse_;
 };
 

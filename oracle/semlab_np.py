@@ -1102,16 +1102,30 @@ class CoarseSolve:
     def __init__(self, space: SemSpace, mode="direct", amg_opts=None):
         self.space, self.mode = space, mode
         self.A, self.free = assemble_p1(space)
+        self.neumann = space.bc == NEUMANN
+        if self.neumann and mode != "direct":
+            raise ValueError("pmg: the Neumann coarse problem is singular; it needs the direct coarse solve")
         if mode == "direct":
             from scipy.sparse.linalg import splu
-            self.lu = splu(self.A.tocsc())
+            A = self.A
+            if self.neumann:  # constants span the nullspace: A + 1 1^T / n is SPD
+                n = A.shape[0]
+                A = A.toarray() + 1.0 / n
+                from scipy.sparse import csc_matrix
+                A = csc_matrix(A)
+            self.lu = splu(A.tocsc())
         else:
             self.amg = AmgHierarchy(self.A, amg_opts)
 
     def solve(self, r):
         z = np.zeros(self.space.n)
         rf = np.asarray(r)[self.free]
-        z[self.free] = self.lu.solve(rf) if self.mode == "direct" else self.amg.vcycle(rf)
+        if self.neumann:  # zero-mean right-hand side and solution (nullspace projection)
+            rf = rf - rf.mean()
+        zf = self.lu.solve(rf) if self.mode == "direct" else self.amg.vcycle(rf)
+        if self.neumann:
+            zf = zf - zf.mean()
+        z[self.free] = zf
         return z
 
 
@@ -1121,11 +1135,17 @@ class Pmg:
     x += P e_C, Chebyshev post-smooth with the same eta."""
 
     def __init__(self, mesh, orders=(7, 3, 1), smoother="jacobi", cheb_order=2,
-                 lmin_mult=0.1, lmax_mult=1.1, coarse="direct", precision=64, seed=0):
+                 lmin_mult=0.1, lmax_mult=1.1, coarse="direct", precision=64, seed=0, bc=DIRICHLET,
+                 cycle="standard"):
+        """smoother: "jacobi" | "ras" | "asm" (Chebyshev) | "ras_plain" | "asm_plain" (one plain
+        application per smoothing step); cycle: "standard" (Alg. 1) | "additive"."""
         if list(orders) != sorted(orders, reverse=True) or orders[-1] != 1 or len(set(orders)) != len(orders):
             raise ValueError("pmg: schedule must be strictly decreasing and end at 1")
         self.orders = tuple(orders)
-        self.spaces = [SemSpace(mesh, q) for q in orders]
+        self.plain = smoother.endswith("_plain")
+        self.additive = cycle == "additive"
+        smoother = smoother[:3] if self.plain else smoother
+        self.spaces = [SemSpace(mesh, q, bc) for q in orders]
         self.levels = []
         for sp_ in self.spaces[:-1]:
             # precision 32 at order 7: the smoother's operator uses FP32-rounded factors, like the
@@ -1137,20 +1157,42 @@ class Pmg:
             else:
                 sch = SchwarzSmoother(sp_, RAS if smoother == "ras" else ASM, precision)
                 S = sch.apply
-            lam = estimate_lambda_max(S, A, sp_.n, 10, seed).value
-            cheb = ChebyshevSmoother(S, A, ChebyParams(cheb_order, lmin_mult, lmax_mult, lam))
+            if self.plain:
+                lam, cheb = 0.0, None
+            else:
+                lam = estimate_lambda_max(S, A, sp_.n, 10, seed).value
+                cheb = ChebyshevSmoother(S, A, ChebyParams(cheb_order, lmin_mult, lmax_mult, lam))
             self.levels.append({"space": sp_, "A": A, "S": S, "lam": lam, "cheb": cheb})
         self.transfers = [Transfer(self.spaces[l], self.spaces[l + 1]) for l in range(len(orders) - 1)]
         self.coarse = CoarseSolve(self.spaces[-1], coarse)
 
+    def _smooth(self, l, b, x):
+        lvl = self.levels[l]
+        if not self.plain:
+            lvl["cheb"].smooth(b, x)
+        elif not x.any():
+            x[:] = lvl["S"](b)
+        else:
+            x += lvl["S"](b - lvl["A"](x))
+        return x
+
     def vcycle(self, b, l=0):
+        if self.additive:
+            return self._additive(b, l)
         if l == len(self.levels):
             return self.coarse.solve(b)
         lvl = self.levels[l]
-        x = np.zeros_like(b)
-        lvl["cheb"].smooth(b, x)
+        x = self._smooth(l, b, np.zeros_like(b))
         r = b - lvl["A"](x)
         ec = self.vcycle(self.transfers[l].restrict(r), l + 1)
         x += self.transfers[l].prolong(ec)
-        lvl["cheb"].smooth(b, x)
+        return self._smooth(l, b, x)
+
+    def _additive(self, b, l=0):
+        """Additive V-cycle: every level smooths its restricted right-hand side from
+        zero, the coarsest is solved, the prolongated corrections are summed; no post-smoothing."""
+        if l == len(self.levels):
+            return self.coarse.solve(b)
+        x = self._smooth(l, b, np.zeros_like(b))
+        x += self.transfers[l].prolong(self._additive(self.transfers[l].restrict(b), l + 1))
         return x

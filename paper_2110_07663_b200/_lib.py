@@ -48,6 +48,12 @@ class GmresStatsC(C.Structure):
                 ("history_len", i32)]
 
 
+class PmgOptionsC(C.Structure):
+    """semlab_pmg_options (SPEC.md:313-349)."""
+    _fields_ = [("smoother", i32), ("cheb_order", i32), ("lambda_min_mult", f64), ("lambda_max_mult", f64),
+                ("precision", i32), ("coarse", i32), ("bc", i32), ("cycle", i32)]
+
+
 MAP_FN = C.CFUNCTYPE(None, p, f64, f64, f64, pf64)
 APPLY_FN = C.CFUNCTYPE(None, p, p, p)
 
@@ -100,6 +106,7 @@ SIGNATURES = {
     "semlab_cheby_destroy": (i32, [p]),
     "semlab_cheby_smooth": (i32, [p, p, p]),
     "semlab_pmg_create": (i32, [p, i32, pi32, i32, i32, f64, f64, i32, i32, C.POINTER(p)]),
+    "semlab_pmg_create_ex": (i32, [p, i32, pi32, C.POINTER(PmgOptionsC), C.POINTER(p)]),
     "semlab_pmg_destroy": (i32, [p]),
     "semlab_pmg_vcycle": (i32, [p, p, p]),
     "semlab_pmg_space": (i32, [p, i32, C.POINTER(p)]),

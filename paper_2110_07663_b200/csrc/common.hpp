@@ -146,6 +146,9 @@ struct DevBuf {
     n = 0;
   }
   void zero(cudaStream_t s) { if (n) SB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+  void download(T* h, size_t count, cudaStream_t s) const {
+    SB_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
   void upload(const T* h, size_t count, cudaStream_t s) {
     SB_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
   }

@@ -98,7 +98,6 @@ static std::vector<double> host_geometry(semlab_space sp) {
 // Element matrices from the reference kernel applied to unit vectors (sem_space.cpp:127-175),
 // assembled like setFromTriplets (duplicates summed in insertion order: ascending element).
 HostCsr assemble_free_matrix(semlab_space sp) {
-  if (sp->bc != SEMLAB_BC_DIRICHLET) invalid("coarse solve: only the Dirichlet problem is supported");
   if (sp->distributed()) invalid("coarse solve: assemble on a whole-mesh space");
   const int q = sp->order, nd = q + 1, nl = nd * nd * nd, nd2 = nd * nd;
   const int64_t E = sp->E;
@@ -106,7 +105,8 @@ HostCsr assemble_free_matrix(semlab_space sp) {
   const double* D = g.diff.data();
   const Slab& sl = sp->sl;
   std::vector<double> geom = host_geometry(sp);
-  const int64_t fx = sl.Nx - 2, fy = sl.Ny - 2, fz = sl.Nz - 2;
+  const int64_t mb = sl.dirichlet ? 1 : 0;  // Dirichlet: the lattice boundary is masked out
+  const int64_t fx = sl.Nx - 2 * mb, fy = sl.Ny - 2 * mb, fz = sl.Nz - 2 * mb;
   const int64_t nfree = fx * fy * fz;
   std::vector<std::vector<std::pair<int, double>>> rows(static_cast<size_t>(nfree));
   std::vector<double> in(static_cast<size_t>(nl)), out(static_cast<size_t>(nl)), ur(static_cast<size_t>(nl)), us(static_cast<size_t>(nl)), ut(static_cast<size_t>(nl));
@@ -157,7 +157,7 @@ HostCsr assemble_free_matrix(semlab_space sp) {
         for (int i = 0; i < nd; ++i) {
           const int64_t x = int64_t(ex) * q + i, y = int64_t(ey) * q + j, z = int64_t(ez) * q + k;
           fidx[size_t(i + nd * j + nd2 * k)] =
-              sl.masked(x, y, z) ? -1 : (x - 1) + fx * ((y - 1) + fy * (z - 1));
+              sl.masked(x, y, z) ? -1 : (x - mb) + fx * ((y - mb) + fy * (z - mb));
         }
     for (int c = 0; c < nl; ++c) {
       if (fidx[size_t(c)] < 0) continue;
@@ -337,6 +337,9 @@ void CoarseSolver::build(semlab_space space, int m) {
   cudaStream_t s = sp->ctx->stream;
   rf.alloc(size_t(nfree));
   zf.alloc(size_t(nfree));
+  neumann = sp->bc == SEMLAB_BC_NEUMANN;
+  if (neumann && mode != SEMLAB_COARSE_DIRECT)
+    invalid("pmg: the Neumann coarse problem is singular; it needs SEMLAB_COARSE_DIRECT (nullspace projection)");
   if (mode == SEMLAB_COARSE_DIRECT) {
     if (nfree > 20000)
       invalid("coarse direct solve is limited to 20000 free dofs (got " + std::to_string(nfree) +
@@ -346,6 +349,10 @@ void CoarseSolver::build(semlab_space space, int m) {
       for (int64_t k = A.ptr[size_t(i)]; k < A.ptr[size_t(i) + 1]; ++k) M[size_t(i) + size_t(nfree) * A.idx[size_t(k)]] = A.val[size_t(k)];
       I[size_t(i) + size_t(nfree) * i] = 1.0;
     }
+    // Neumann: A has the constants as its nullspace. A + 1 1^T / n is SPD and,
+    // on zero-mean right-hand sides, has the zero-mean solution of A e = r.
+    if (neumann)
+      for (auto& v : M) v += 1.0 / double(nfree);
     DevBuf<double> dM(M.size());
     Minv.alloc(I.size());
     dM.upload(M.data(), M.size(), s);
@@ -364,6 +371,26 @@ void CoarseSolver::build(semlab_space space, int m) {
     sp->ctx->sync();
     cusolverDnDestroy(h);
     if (hinfo != 0) numeric("coarse solve: factorization failed (info " + std::to_string(hinfo) + ")");
+    if (neumann) {  // e = Pi M^-1 Pi r with Pi = I - 1 1^T / n: the mean of e is 0
+      std::vector<double> H(I.size());
+      Minv.download(H.data(), H.size(), s);
+      sp->ctx->sync();
+      const int64_t nn = nfree;
+      std::vector<double> rm(size_t(nn), 0.0), cm(size_t(nn), 0.0);
+      double tm = 0.0;
+      for (int64_t j = 0; j < nn; ++j)
+        for (int64_t i = 0; i < nn; ++i) {
+          const double v = H[size_t(i + nn * j)];
+          rm[size_t(i)] += v;
+          cm[size_t(j)] += v;
+          tm += v;
+        }
+      for (int64_t j = 0; j < nn; ++j)
+        for (int64_t i = 0; i < nn; ++i)
+          H[size_t(i + nn * j)] += -rm[size_t(i)] / double(nn) - cm[size_t(j)] / double(nn) + tm / double(nn * nn);
+      Minv.upload(H.data(), H.size(), s);
+      sp->ctx->sync();
+    }
     return;
   }
   // AMG (amg.cpp:69-129): host setup, device V-cycle
@@ -526,12 +553,16 @@ void semlab_pmg_s::build() {
     sp->ctx = ctx;
     sp->mesh = mesh;
     sp->order = orders[l];
-    sp->bc = SEMLAB_BC_DIRICHLET;
+    sp->bc = bc;
     sp->build();
     L.sp = sp.release();
     const int64_t n = L.sp->n;
     L.b.alloc(size_t(n));
     L.x.alloc(size_t(n));
+    if (plain()) {
+      L.t.alloc(size_t(n));
+      L.t.zero(ctx->stream);
+    }
     L.r.alloc(size_t(n));
     L.b.zero(ctx->stream);
     L.x.zero(ctx->stream);
@@ -555,13 +586,15 @@ void semlab_pmg_s::build() {
     } else {
       auto sch = std::make_unique<semlab_schwarz_s>();
       sch->space = L.sp;
-      sch->mode = smoother == SEMLAB_SMOOTHER_RAS ? SEMLAB_SCHWARZ_RAS : SEMLAB_SCHWARZ_ASM;
+      sch->mode = (smoother == SEMLAB_SMOOTHER_RAS || smoother == SEMLAB_SMOOTHER_RAS_PLAIN) ? SEMLAB_SCHWARZ_RAS
+                                                                                             : SEMLAB_SCHWARZ_ASM;
       sch->precision = precision;
       sch->build();
       L.sch = sch.release();
       L.S->kind = semlab_op_s::kSchwarz;
       L.S->sch = L.sch;
     }
+    if (plain()) continue;  // un-accelerated smoothers: no Chebyshev, no lambda estimate
     L.lam = estimate_lambda_max(L.S, L.A, n, 10, 0).value;
     if (!(L.lam > 0.0)) numeric("pmg: lambda estimate failed on level " + std::to_string(l));
     semlab_cheby_params p{cheb_order, lmin, lmax, L.lam};
@@ -586,7 +619,7 @@ void semlab_pmg_s::build() {
     full->ctx = ctx;
     full->mesh = mesh;
     full->order = orders.back();
-    full->bc = SEMLAB_BC_DIRICHLET;
+    full->bc = bc;
     full->full = true;
     full->build();
     coarse_full = full.release();
@@ -644,7 +677,6 @@ void semlab_pmg_s::restrict_(int l, const double* fv, double* cv, const double* 
 // Alg. 1 with x0 = 0: pre-smooth, residual, restrict, recurse, correct, post-smooth.
 void semlab_pmg_s::cycle(int l) {
   Level& L = lv[size_t(l)];
-  cudaStream_t s = ctx->stream;
   if (l == int(lv.size()) - 1) {
     if (coarse_full)
       coarse.solve_dist(L.sp, L.b.p, L.x.p);
@@ -652,16 +684,54 @@ void semlab_pmg_s::cycle(int l) {
       coarse.solve(L.b.p, L.x.p);
     return;
   }
-  const int64_t n = L.sp->n;
-  SB_CUDA(cudaMemsetAsync(L.x.p, 0, size_t(n) * sizeof(double), s));
-  L.cheb->smooth(L.b.p, L.x.p, true);
+  smooth(l, true);
   // r = b - A x is not stored: the first restriction pass reads b and A x (bitwise the same
   // b - Ax), so the Ax keeps the plain-write epilogue
   L.sp->apply_A(L.x.p, L.r.p, L.A->geom32);  // (+ the interface-plane sum on a slab)
   restrict_(l, L.r.p, lv[size_t(l) + 1].b.p, L.b.p);
   cycle(l + 1);
   prolong(l, lv[size_t(l) + 1].x.p, L.x.p, true);  // x += P e_C (fused into the last pass)
-  L.cheb->smooth(L.b.p, L.x.p, false);
+  smooth(l, false);
+}
+
+// One smoothing step on level l: Chebyshev(eta) of the level's S (chebyshev.cpp:76-96), or the
+// un-accelerated smoother: x = S b from x = 0, else x += S (b - A x).
+void semlab_pmg_s::smooth(int l, bool x_is_zero) {
+  Level& L = lv[size_t(l)];
+  cudaStream_t s = ctx->stream;
+  const int64_t n = L.sp->n;
+  if (x_is_zero) SB_CUDA(cudaMemsetAsync(L.x.p, 0, size_t(n) * sizeof(double), s));
+  if (!plain()) {
+    L.cheb->smooth(L.b.p, L.x.p, x_is_zero);
+    return;
+  }
+  if (x_is_zero) {
+    L.S->apply(L.b.p, L.x.p);
+    return;
+  }
+  L.sp->apply_A(L.x.p, L.r.p, L.A->geom32);
+  ctx->count(launch_sub(L.r.p, L.b.p, L.r.p, n, s));  // r = b - A x
+  L.S->apply(L.r.p, L.t.p);
+  ctx->count(launch_axpby(L.x.p, 1.0, L.t.p, 1.0, n, s));
+}
+
+// Additive V-cycle (§2.2.2 "an additive V-cycle with no post-smoothing is
+// used to avoid residual re-evaluation"): every level smooths its restricted right-hand side
+// b_{l+1} = P^T b_l from x = 0, the coarsest level is solved, and the corrections are summed
+// upwards, x_l += P x_{l+1}. No residual is re-evaluated and there is no post-smoothing.
+void semlab_pmg_s::cycle_additive(int l) {
+  Level& L = lv[size_t(l)];
+  if (l == int(lv.size()) - 1) {
+    if (coarse_full)
+      coarse.solve_dist(L.sp, L.b.p, L.x.p);
+    else
+      coarse.solve(L.b.p, L.x.p);
+    return;
+  }
+  restrict_(l, L.b.p, lv[size_t(l) + 1].b.p);
+  smooth(l, true);
+  cycle_additive(l + 1);
+  prolong(l, lv[size_t(l) + 1].x.p, L.x.p, true);
 }
 
 // SEMLAB_PMG_GRAPH=0 launches the V-cycle kernel by kernel instead of as a CUDA graph.
@@ -680,11 +750,11 @@ static bool pmg_graph_enabled() {
 void semlab_pmg_s::run_cycle() {
   cudaStream_t s = ctx->stream;
   if (!pmg_graph_enabled() || graph_state < 0) {
-    cycle(0);
+    run_body();
     return;
   }
   if (graph_state == 0) {  // eager warm-up
-    cycle(0);
+    run_body();
     graph_state = 1;
     return;
   }
@@ -694,7 +764,7 @@ void semlab_pmg_s::run_cycle() {
     bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
       try {
-        cycle(0);
+        run_body();
       } catch (...) {
         ok = false;
       }
@@ -707,13 +777,20 @@ void semlab_pmg_s::run_cycle() {
     if (!ok) {
       (void)cudaGetLastError();
       graph_state = -1;  // not capturable here: stay eager
-      cycle(0);
+      run_body();
       return;
     }
     graph_state = 2;
   }
   SB_CUDA(cudaGraphLaunch(graph_exec, s));
   ctx->count(graph_launches);
+}
+
+void semlab_pmg_s::run_body() {
+  if (cycle_mode == SEMLAB_CYCLE_ADDITIVE)
+    cycle_additive(0);
+  else
+    cycle(0);
 }
 
 void semlab_pmg_s::vcycle(const double* b, double* z) {
@@ -725,28 +802,46 @@ void semlab_pmg_s::vcycle(const double* b, double* z) {
 
 extern "C" {
 
-int semlab_pmg_create(semlab_mesh mesh, int nlevels, const int* orders, int smoother, int cheb_order, double lmin,
-                      double lmax, int precision, int coarse, semlab_pmg* out) {
+int semlab_pmg_create_ex(semlab_mesh mesh, int nlevels, const int* orders, const semlab_pmg_options* o,
+                         semlab_pmg* out) {
   return guard([&] {
     need(mesh, "pmg: mesh");
     need(orders, "pmg: orders");
+    need(o, "pmg: options");
     need(out, "pmg: out");
-    if (smoother < 0 || smoother > 2) invalid("pmg: unknown smoother");
-    if (coarse != SEMLAB_COARSE_DIRECT && coarse != SEMLAB_COARSE_AMG) invalid("pmg: unknown coarse solver");
-    if (precision != 32 && precision != 64) invalid("pmg: precision must be 32 or 64");
+    if (o->smoother < 0 || o->smoother > SEMLAB_SMOOTHER_ASM_PLAIN) invalid("pmg: unknown smoother");
+    if (o->coarse != SEMLAB_COARSE_DIRECT && o->coarse != SEMLAB_COARSE_AMG) invalid("pmg: unknown coarse solver");
+    if (o->precision != 32 && o->precision != 64) invalid("pmg: precision must be 32 or 64");
+    if (o->bc != SEMLAB_BC_DIRICHLET && o->bc != SEMLAB_BC_NEUMANN) invalid("pmg: unknown boundary condition");
+    if (o->cycle != SEMLAB_CYCLE_STANDARD && o->cycle != SEMLAB_CYCLE_ADDITIVE) invalid("pmg: unknown cycle");
     auto p = std::make_unique<semlab_pmg_s>();
     p->ctx = mesh->ctx;
     p->mesh = mesh;
     p->orders.assign(orders, orders + nlevels);
-    p->smoother = smoother;
-    p->cheb_order = cheb_order;
-    p->lmin = lmin;
-    p->lmax = lmax;
-    p->precision = precision;
-    p->coarse_mode = coarse;
+    p->smoother = o->smoother;
+    p->cheb_order = o->cheb_order;
+    p->lmin = o->lambda_min_mult;
+    p->lmax = o->lambda_max_mult;
+    p->precision = o->precision;
+    p->coarse_mode = o->coarse;
+    p->bc = o->bc;
+    p->cycle_mode = o->cycle;
+    // the Neumann mean removal synchronises the host (reductions): those cycles run eagerly
+    if (p->bc == SEMLAB_BC_NEUMANN) p->graph_state = -1;
     p->build();
     *out = p.release();
   });
+}
+
+int semlab_pmg_create(semlab_mesh mesh, int nlevels, const int* orders, int smoother, int cheb_order, double lmin,
+                      double lmax, int precision, int coarse, semlab_pmg* out) {
+  if (smoother < 0 || smoother > SEMLAB_SMOOTHER_ASM) {
+    sb_set_error("pmg: unknown smoother");
+    return SEMLAB_EINVAL;
+  }
+  const semlab_pmg_options o{smoother, cheb_order, lmin, lmax, precision, coarse, SEMLAB_BC_DIRICHLET,
+                             SEMLAB_CYCLE_STANDARD};
+  return semlab_pmg_create_ex(mesh, nlevels, orders, &o, out);
 }
 
 int semlab_pmg_destroy(semlab_pmg p) {

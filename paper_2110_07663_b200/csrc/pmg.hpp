@@ -56,6 +56,7 @@ struct CoarseSolver {
   int64_t coarse_n = 0;
   double omega = 0.9;
   DevBuf<double> gsend, grecv, rfull, zfull;  // distributed gather of the coarse residual
+  bool neumann = false;  // singular coarse problem: solve on the zero-mean subspace
   void build(semlab_space space, int mode);
   void solve(const double* r_full, double* z_full);
   void solve_dist(semlab_space dist_space, const double* r_loc, double* z_loc);
@@ -69,6 +70,8 @@ struct semlab_pmg_s {
   semlab_mesh mesh = nullptr;
   std::vector<int> orders;
   int smoother = SEMLAB_SMOOTHER_JACOBI, cheb_order = 2, precision = 32, coarse_mode = SEMLAB_COARSE_DIRECT;
+  int bc = SEMLAB_BC_DIRICHLET, cycle_mode = SEMLAB_CYCLE_STANDARD;
+  bool plain() const { return smoother == SEMLAB_SMOOTHER_RAS_PLAIN || smoother == SEMLAB_SMOOTHER_ASM_PLAIN; }
   double lmin = 0.1, lmax = 1.1;
   struct Level {
     semlab_space sp = nullptr;
@@ -76,7 +79,7 @@ struct semlab_pmg_s {
     semlab_op A = nullptr, S = nullptr;
     semlab_cheby cheb = nullptr;
     double lam = 0.0;
-    sb::DevBuf<double> b, x, r;
+    sb::DevBuf<double> b, x, r, t;
   };
   std::vector<Level> lv;
   std::vector<sb::Jmat> J;  // J[l]: level l+1 (coarse) -> level l (fine)
@@ -89,6 +92,9 @@ struct semlab_pmg_s {
   void restrict_(int l, const double* fine_v, double* coarse_v, const double* sub_from = nullptr);  // Pᵀ (sub_from - fine_v) if given
   void vcycle(const double* b, double* z);
   void cycle(int l);
+  void cycle_additive(int l);
+  void run_body();  // cycle(0) or cycle_additive(0)
+  void smooth(int l, bool x_is_zero);  // x_l <- smoother(b_l, x_l)
   void run_cycle();  // cycle(0), replayed as a captured CUDA graph after one eager call
   cudaGraphExec_t graph_exec = nullptr;
   int graph_state = 0;  // 0 not run, 1 warmed up, 2 captured, -1 eager only

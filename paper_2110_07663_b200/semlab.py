@@ -20,7 +20,8 @@ from ._lib import check, lib
 
 DIRICHLET, NEUMANN = 0, 1          # BcMode, sem_space.hpp:12
 ASM, RAS = 0, 1                    # SchwarzMode, schwarz.hpp:10
-JACOBI_SMOOTHER, RAS_SMOOTHER, ASM_SMOOTHER = 0, 1, 2
+JACOBI_SMOOTHER, RAS_SMOOTHER, ASM_SMOOTHER, RAS_PLAIN_SMOOTHER, ASM_PLAIN_SMOOTHER = 0, 1, 2, 3, 4
+STANDARD_CYCLE, ADDITIVE_CYCLE = 0, 1
 COARSE_DIRECT, COARSE_AMG = 0, 1
 
 
@@ -405,19 +406,24 @@ class Pmg:
     """p-multigrid V-cycle preconditioner (RESTATED: pmg.cpp missing)."""
 
     def __init__(self, mesh: HexMesh, orders=(7, 3, 1), smoother: int = JACOBI_SMOOTHER, cheb_order: int = 2,
-                 lmin_mult: float = 0.1, lmax_mult: float = 1.1, precision: int = 32, coarse: int = COARSE_DIRECT):
-        self.mesh, self.orders = mesh, tuple(orders)
+                 lmin_mult: float = 0.1, lmax_mult: float = 1.1, precision: int = 32, coarse: int = COARSE_DIRECT,
+                 bc: int = DIRICHLET, cycle: int = STANDARD_CYCLE):
+        """smoother: Chebyshev-{Jacobi, RAS, ASM} or plain (un-accelerated) RAS / ASM; cycle: Alg. 1
+        (standard) or additive (no post-smoothing); bc=NEUMANN builds every level in Neumann mode
+        and solves the coarse problem on the zero-mean subspace (direct coarse solve)."""
+        self.mesh, self.orders, self.bc = mesh, tuple(orders), bc
         arr = (C.c_int * len(orders))(*orders)
         h = C.c_void_p()
-        check(lib.semlab_pmg_create(mesh.handle, len(orders), arr, int(smoother), int(cheb_order), float(lmin_mult),
-                                    float(lmax_mult), int(precision), int(coarse), C.byref(h)))
+        opts = _lib.PmgOptionsC(int(smoother), int(cheb_order), float(lmin_mult), float(lmax_mult), int(precision),
+                                int(coarse), int(bc), int(cycle))
+        check(lib.semlab_pmg_create_ex(mesh.handle, len(orders), arr, C.byref(opts), C.byref(h)))
         self.handle = h
         _own(self, h, lib.semlab_pmg_destroy, mesh)
         self.spaces = []
         for lvl in range(len(orders)):
             sh = C.c_void_p()
             check(lib.semlab_pmg_space(h, lvl, C.byref(sh)))
-            self.spaces.append(_BorrowedSpace(sh, mesh, orders[lvl], self))
+            self.spaces.append(_BorrowedSpace(sh, mesh, orders[lvl], self, bc))
         self.n = self.spaces[0].n
 
     def lam(self, level: int) -> float:
@@ -461,8 +467,8 @@ class _BorrowedSpace(SemSpace):
     Pmg alive (self._owner), and objects built on it (smoothers, operators) register as children
     of the Pmg's box, so they are released before the hierarchy frees the space."""
 
-    def __init__(self, handle, mesh, order, owner):
-        self.mesh, self.order, self.bc, self.ctx = mesh, order, DIRICHLET, mesh.ctx
+    def __init__(self, handle, mesh, order, owner, bc=DIRICHLET):
+        self.mesh, self.order, self.bc, self.ctx = mesh, order, bc, mesh.ctx
         self._owner = owner
         self._box = owner._box
         self.handle = None

@@ -115,3 +115,23 @@ def test_projection_basis_pinned():
     Vb = np.stack(pb.basis, axis=1)
     gram = Vb.T @ np.stack([s.apply_A(v) for v in pb.basis], axis=1)
     assert np.abs(gram - np.eye(3)).max() < 1e-12
+
+
+PMG_EXT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "pmg_ext_golden.npz")
+
+
+@pytest.mark.parametrize("name", ["ras_plain_std", "asm_plain_add", "ras_plain_add", "ras_cheb_add",
+                                  "neu_ras_cheb_std", "neu_jac_cheb_std", "neu_asm_plain_add"])
+def test_pmg_variants_pinned(name):
+    """Plain ASM/RAS smoothers, the additive V-cycle and the Neumann hierarchy:
+    the numpy restatement against the reference classes under oracle/ref_ext's pMG."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_golden_pmg import VCYCLES
+    g = np.load(PMG_EXT)
+    eps, E, orders, sm, coarse, eta, neu, add = VCYCLES[name]
+    pmg = o.Pmg(o.generate_kershaw(eps, E), orders, sm, eta, 0.1, 1.1, coarse, 64,
+                bc=o.NEUMANN if neu else o.DIRICHLET, cycle="additive" if add else "standard")
+    z = pmg.vcycle(g[f"vc_{name}_b"])
+    want = g[f"vc_{name}_z"]
+    assert np.abs(z - want).max() <= 1e-10 * np.abs(want).max()
