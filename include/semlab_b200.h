@@ -38,6 +38,11 @@ const char* semlab_version(void);
    (fused Ax, warp-per-element RAS) at max_ctas CTAs so every warp runs many elements even on a
    small mesh; results must not change. 0 restores the occupancy-sized grid. Process-wide. */
 int semlab_debug_set_grid_cap(int max_ctas);
+/* GMRES form (process-wide): 1 (default) keeps the preconditioned directions Z and updates
+   x += Z y when device memory allows (flexible GMRES: equal to the reference's x += M (V y) for a
+   linear M, one M fewer per cycle, and robust to the FP32 smoother); 0 always uses the
+   reference's x += M (V y) (krylov.cpp:108-114), as the solver does when Z does not fit. */
+int semlab_debug_set_gmres_form(int flexible);
 
 /* ---- opaque handles ---------------------------------------------------------------------- */
 typedef struct semlab_ctx_s* semlab_ctx;         /* device + stream (+ NCCL communicator)  */

@@ -62,6 +62,7 @@ SIGNATURES = {
     "semlab_last_error": (C.c_char_p, []),
     "semlab_version": (C.c_char_p, []),
     "semlab_debug_set_grid_cap": (i32, [i32]),
+    "semlab_debug_set_gmres_form": (i32, [i32]),
     "semlab_ctx_create": (i32, [i32, p, C.POINTER(p)]),
     "semlab_ctx_create_dist": (i32, [i32, p, i32, i32, p, C.POINTER(p)]),
     "semlab_nccl_get_unique_id": (i32, [p]),

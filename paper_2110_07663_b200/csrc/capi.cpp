@@ -28,8 +28,12 @@ int g_ctx_device = -1;  // the one device this process's contexts use
 int g_ctx_live = 0;
 }  // namespace
 
+namespace {
+std::atomic<int> g_gmres_flexible{1};
+}
 namespace sb {
 int grid_cap() { return g_grid_cap.load(std::memory_order_relaxed); }
+bool gmres_flexible_allowed() { return g_gmres_flexible.load(std::memory_order_relaxed) != 0; }
 
 int per_device_once(const void* key, const std::function<int()>& init) {
   static std::mutex mu;
@@ -65,6 +69,10 @@ extern "C" {
 
 const char* semlab_last_error(void) { return g_err.c_str(); }
 const char* semlab_version(void) { return "semlab_b200 0.2 (sm_100a)"; }
+
+int semlab_debug_set_gmres_form(int flexible) {
+  return guard([&] { g_gmres_flexible.store(flexible ? 1 : 0); });
+}
 
 int semlab_debug_set_grid_cap(int max_ctas) {
   return guard([&] {

@@ -68,6 +68,8 @@ void smem_attr(K kern, size_t smem) {
     return 1;
   });
 }
+// Test/debug: false forces GMRES to the reference's x += M (V y) form (semlab_debug_set_gmres_form).
+bool gmres_flexible_allowed();
 inline int capped_grid(int64_t grid) {
   const int c = grid_cap();
   return int(c > 0 && grid > c ? c : grid);

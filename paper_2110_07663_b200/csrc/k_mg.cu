@@ -152,11 +152,13 @@ int64_t launch_transfer_pass(bool prolong, const double* in, const Grid3& gin, d
 
 // ---------------------------------------------------------------- free-dof maps (Dirichlet p=1)
 // free index f = (x-1) + (Nx-2)((y-1) + (Ny-2)(z-1)); lattice vector uses the space layout.
+// Free dofs: the lattice interior (Dirichlet: the boundary is masked) or the whole lattice (Neumann).
 int64_t launch_gather_free(const Slab& sl, const double* full, double* freev, cudaStream_t s) {
-  const int64_t fx = sl.Nx - 2, fy = sl.Ny - 2, fz = sl.Nz - 2;
+  const int64_t mb = sl.dirichlet ? 1 : 0;
+  const int64_t fx = sl.Nx - 2 * mb, fy = sl.Ny - 2 * mb, fz = sl.Nz - 2 * mb;
   const Slab g = sl;
   auto body = [=] __device__(int64_t f) {
-    const int64_t x = 1 + f % fx, y = 1 + (f / fx) % fy, z = 1 + f / (fx * fy);
+    const int64_t x = mb + f % fx, y = mb + (f / fx) % fy, z = mb + f / (fx * fy);
     freev[f] = full[g.lidx(x, y, z)];
   };
   const int64_t n = fx * fy * fz;
@@ -167,12 +169,13 @@ int64_t launch_gather_free(const Slab& sl, const double* full, double* freev, cu
 }
 
 int64_t launch_scatter_free(const Slab& sl, const double* freev, double* full, cudaStream_t s) {
-  const int64_t fx = sl.Nx - 2, fy = sl.Ny - 2;
+  const int64_t mb = sl.dirichlet ? 1 : 0;
+  const int64_t fx = sl.Nx - 2 * mb, fy = sl.Ny - 2 * mb;
   const Slab g = sl;
   const int64_t n = g.n_local();
   auto body = [=] __device__(int64_t t) {
     const int64_t x = t % g.Nx, y = (t / g.Nx) % g.Ny, z = g.zlo + t / (g.Nx * g.Ny);
-    full[t] = g.masked(x, y, z) ? 0.0 : freev[(x - 1) + fx * ((y - 1) + fy * (z - 1))];
+    full[t] = g.masked(x, y, z) ? 0.0 : freev[(x - mb) + fx * ((y - mb) + fy * (z - mb))];
   };
   k_foreach_mg<<<grid_for(n), 256, 0, s>>>(n, body);
   SB_LAUNCH_CHECK();

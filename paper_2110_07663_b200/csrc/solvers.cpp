@@ -368,14 +368,29 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
   // ~1e-7) it keeps the least-squares residual estimate consistent with the true residual, so
   // the FP32-smoothed solve needs the FP64 solve's iteration count instead of an extra restart.
   const int nb = cgs2_stride(m + 1);
-  const int zc = M ? m : 0;
+  // Flexible form (Z kept) when the device has room for the m extra columns; otherwise (e.g. one
+  // B200 at E = 96^3, where Z alone is 49 GB) the reference's x += M (V y), one extra M per cycle.
+  bool flexible = M != nullptr && gmres_flexible_allowed();
+  if (flexible) {
+    const size_t need = (size_t(ld) * (2 * m + 3) + size_t(3 * nb)) * sizeof(double);
+    const size_t have = c->krylov_ws_busy ? 0 : c->krylov_ws.n * sizeof(double);
+    if (need > have) {
+      size_t free_b = 0, total_b = 0;
+      SB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      flexible = need - have + (size_t(2) << 30) <= free_b;
+    }
+  }
+  const int zc = flexible ? m : 0;
   WsLease ws(c, size_t(ld) * (m + 3 + zc) + size_t(3 * nb));
   struct {
     double* p;
   } r{ws.p}, w{ws.p + ld}, V{ws.p + 2 * ld}, Z{ws.p + size_t(ld) * (m + 3)},
       dh{ws.p + size_t(ld) * (m + 3 + zc)};
-  // z_j: stored column of Z, or v_j itself without a preconditioner
-  auto dir = [&](int j) { return M ? Z.p + size_t(j) * ld : V.p + size_t(j) * ld; };
+  // z_j: stored column of Z (flexible), else a single scratch column (the reference form), or v_j
+  // itself without a preconditioner
+  auto dir = [&](int j) {
+    return flexible ? Z.p + size_t(j) * ld : (M ? w.p : V.p + size_t(j) * ld);
+  };
   auto norm = [&](const double* v) {
     const double* av[1] = {v};
     double r2 = 0.0;
@@ -405,8 +420,15 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
     int j = 0;
     bool lucky = false;
     for (; j < m && res.iterations < cfg.max_iters; ++j) {
-      if (M) M->apply(V.p + size_t(j) * ld, dir(j));
-      A->apply(dir(j), w.p);
+      if (flexible) {
+        M->apply(V.p + size_t(j) * ld, dir(j));
+        A->apply(dir(j), w.p);
+      } else if (M) {  // z_j is not kept: M v_j in r's column (r is free until the cycle ends)
+        M->apply(V.p + size_t(j) * ld, r.p);
+        A->apply(r.p, w.p);
+      } else {
+        A->apply(dir(j), w.p);
+      }
       double hnext = 0.0;
       cgs2(c, o, V.p, ld, j + 1, w.p, dh.p, nb, h, hnext);
       for (int i = 0; i <= j; ++i) Hc(i, j) = h[size_t(i)];
@@ -445,7 +467,13 @@ KrylovResult gmres_solve(semlab_op A, semlab_op M, const double* b, double* x, c
         for (int k = i + 1; k < j; ++k) acc -= Hc(i, k) * y[size_t(k)];
         y[size_t(i)] = acc / Hc(i, i);
       }
-      c->count(launch_gemv_n(dir(0), ld, j, y.data(), x, n, s, true));
+      if (flexible || !M) {
+        c->count(launch_gemv_n(dir(0), ld, j, y.data(), x, n, s, true));
+      } else {  // x += M (V y), krylov.cpp:108-114
+        c->count(launch_gemv_n(V.p, ld, j, y.data(), w.p, n, s));
+        M->apply(w.p, r.p);
+        c->count(launch_axpby(x, 1.0, r.p, 1.0, n, s));
+      }
     }
     A->apply(x, r.p);
     c->count(launch_sub(r.p, b, r.p, n, s));

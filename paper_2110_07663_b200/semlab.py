@@ -586,6 +586,11 @@ def debug_set_grid_cap(max_ctas: int) -> None:
     check(lib.semlab_debug_set_grid_cap(int(max_ctas)))
 
 
+def debug_set_gmres_form(flexible: bool) -> None:
+    """False: GMRES always uses the reference's x += M (V y) (as when Z does not fit in memory)."""
+    check(lib.semlab_debug_set_gmres_form(1 if flexible else 0))
+
+
 def host_gll(order: int):
     n = order + 1
     nodes, w, d = np.zeros(n), np.zeros(n), np.zeros(n * n)

@@ -132,3 +132,30 @@ def test_lambda_estimate_many_rounds(ctx):
     got = S.estimate_lambda_max(g.jacobi(), g.as_linop(), g.n, 40, 0)
     assert got.rounds_used == want.rounds_used
     assert abs(got.value - want.value) <= 1e-9 * want.value
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_gmres_reference_form_matches_flexible(ctx, precision):
+    """When the Z basis does not fit (one B200 at E=96^3) GMRES falls back to the reference's own
+    x += M (V y) update. FP64 smoother: same iterations, x to 1e-10 of the flexible form. FP32
+    smoother: the reference form may need a restart more (the V-cycle is linear only to ~1e-7)."""
+    from paper_2110_07663_b200 import semlab as S
+    pmg = S.Pmg(S.generate_kershaw(0.3, 4, ctx), (7, 3, 1), S.RAS_SMOOTHER, 2, 0.1, 1.1, precision)
+    sp = pmg.spaces[0]
+    b = sp.build_rhs(1)
+    x_flex, x_ref = sp.zeros(), sp.zeros()
+    st_f = S.gmres_solve(sp.as_linop(), pmg.as_linop(), b, x_flex)
+    S.debug_set_gmres_form(False)
+    try:
+        st_r = S.gmres_solve(sp.as_linop(), pmg.as_linop(), b, x_ref)
+    finally:
+        S.debug_set_gmres_form(True)
+    c = o.Pmg(o.generate_kershaw(0.3, 4), (7, 3, 1), "ras", 2, 0.1, 1.1, "direct", precision)
+    cs = c.spaces[0]
+    xo = np.zeros(cs.n)
+    st_o = o.gmres_solve(cs.apply_A, c.vcycle, o.build_rhs(cs, 1), xo, o.GmresConfig())
+    assert st_f.converged and st_r.converged
+    assert abs(st_r.iterations - st_o.iterations) <= 1  # the oracle runs the reference form too
+    if precision == 64:
+        assert abs(st_f.iterations - st_r.iterations) <= 1
+        assert rel(x_ref, xo) < 1e-10
