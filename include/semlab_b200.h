@@ -54,6 +54,7 @@ typedef struct semlab_cheby_s* semlab_cheby;     /* ChebyshevSmoother, chebyshev
 typedef struct semlab_proj_s* semlab_proj;       /* ProjectionBasis, krylov.hpp:39-59      */
 typedef struct semlab_pmg_s* semlab_pmg;         /* pMG hierarchy (pmg.cpp is MISSING in the
                                                     reference; API of SPEC.md:313-349)     */
+typedef struct semlab_semfem_s* semlab_semfem;   /* SemfemPreconditioner, semfem.hpp:36-54 */
 
 /* ---- enums (values mirror the reference enums) -------------------------------------------- */
 #define SEMLAB_BC_DIRICHLET 0 /* BcMode::Dirichlet, sem_space.hpp:12 */
@@ -234,6 +235,18 @@ int semlab_pmg_lambda(semlab_pmg p, int level, double* out);
 /* P (coarse level+1 -> level) and P^T, device vectors of the two levels' spaces. */
 int semlab_pmg_prolong(semlab_pmg p, int level, const double* d_coarse, double* d_fine);
 int semlab_pmg_restrict(semlab_pmg p, int level, const double* d_fine, double* d_coarse);
+
+/* ---- SEMFEM preconditioner (semfem.hpp:14-54) ----------------------------------------------- */
+/* SemfemPreconditioner(space, SemfemInner::Amg), semfem.cpp:112-124: the linear-tetrahedral
+   lattice matrix (assemble_semfem, semfem.cpp:12-98, bitwise the reference's) and its AMG
+   hierarchy (amg.cpp:69-129; host setup, device cycle). Single-rank (whole-mesh) spaces. */
+int semlab_semfem_create(semlab_space s, semlab_semfem* out);
+int semlab_semfem_destroy(semlab_semfem p);
+/* apply, semfem.cpp:127-134: z = mask(one AMG V-cycle of r). */
+int semlab_semfem_apply(semlab_semfem p, const double* d_r, double* d_z);
+/* AMG level sizes (AmgHierarchy::n_levels / level_size) */
+int semlab_semfem_levels(semlab_semfem p, int* nlevels, int64_t* sizes, int cap);
+int semlab_op_semfem(semlab_semfem p, semlab_op* out); /* SemfemPreconditioner::as_linop */
 
 /* ---- Krylov (krylov.hpp:9-33) -------------------------------------------------------------- */
 /* gmres_solve(A, M, b, x, config), krylov.cpp:20-129. M may be NULL (identity). */

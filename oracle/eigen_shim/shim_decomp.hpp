@@ -386,6 +386,22 @@ class SparseMatrix {  // compressed rows, ascending columns
   Index cols() const { return c; }
   Index nonZeros() const { return Index(val.size()); }
   void makeCompressed() {}
+  void prune(S reference, S epsilon) {  // keep |v| > |reference| * epsilon (Eigen's isMuchSmallerThan)
+    std::vector<Index> np{0};
+    std::vector<Index> ni;
+    std::vector<S> nv;
+    for (Index i = 0; i < r; ++i) {
+      for (Index k = ptr[size_t(i)]; k < ptr[size_t(i) + 1]; ++k)
+        if (!(std::abs(val[size_t(k)]) <= std::abs(reference) * epsilon)) {
+          ni.push_back(idx[size_t(k)]);
+          nv.push_back(val[size_t(k)]);
+        }
+      np.push_back(Index(ni.size()));
+    }
+    ptr.swap(np);
+    idx.swap(ni);
+    val.swap(nv);
+  }
   S coeff(Index i, Index j) const {
     auto b = idx.begin() + ptr[size_t(i)], e = idx.begin() + ptr[size_t(i) + 1];
     auto it = std::lower_bound(b, e, j);
@@ -417,7 +433,8 @@ class SparseMatrix {  // compressed rows, ascending columns
   SparseTransposed<S, Opt> transpose() const { return SparseTransposed<S, Opt>{this}; }
   class InnerIterator {
    public:
-    InnerIterator(const SparseMatrix& m, Index i) : m_(m), k_(m.ptr[size_t(i)]), end_(m.ptr[size_t(i) + 1]) {}
+    InnerIterator(const SparseMatrix& m, Index i) : m_(m), i_(i), k_(m.ptr[size_t(i)]), end_(m.ptr[size_t(i) + 1]) {}
+    Index row() const { return i_; }
     explicit operator bool() const { return k_ < end_; }
     InnerIterator& operator++() { ++k_; return *this; }
     Index col() const { return m_.idx[size_t(k_)]; }
@@ -426,7 +443,7 @@ class SparseMatrix {  // compressed rows, ascending columns
 
    private:
     const SparseMatrix& m_;
-    Index k_, end_;
+    Index i_, k_, end_;
   };
 };
 

@@ -5,6 +5,7 @@
 #include <random>
 
 #include "ref_ext.hpp"
+#include "semlab/semfem.hpp"
 
 using namespace semlab;
 using namespace semlab_ref;
@@ -416,6 +417,61 @@ int ref_solve_ex(double eps, int E, const int* orders, int nlev, const char* smo
     cfg.tol = tol;
     const GmresStats st = gmres_solve(A, M, bv, xv, cfg);
     std::memcpy(x, xv.data(), sizeof(double) * size_t(s0->n()));
+    *iters = st.iterations;
+    *rel_res = st.rel_residual;
+  });
+}
+
+// SEMFEM preconditioner (semfem.cpp:12-134), AMG inner solve: z = M r, and the AMG level sizes.
+int ref_semfem_apply(double eps, int E, int p, const double* r, double* z, int* nlev, int64_t* sizes, int cap) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    SemfemPreconditioner pc(s, SemfemInner::Amg);
+    FieldVector rv = Eigen::Map<const Eigen::MatrixXd>(r, s.n(), 1), zv;
+    pc.apply(rv, zv);
+    std::memcpy(z, zv.data(), sizeof(double) * size_t(s.n()));
+    const AmgHierarchy* h = pc.hierarchy();
+    *nlev = h->n_levels();
+    for (int l = 0; l < h->n_levels() && l < cap; ++l) sizes[l] = h->level_size(l);
+  });
+}
+
+// assemble_semfem (semfem.cpp:12-98) as CSR: ptr (n+1), idx/val (cap entries); *nnz set always.
+int ref_semfem_matrix(double eps, int E, int p, int64_t* nnz, int64_t* ptr, int64_t* idx, double* val, int64_t cap) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    const CsrMatrix A = assemble_semfem(s);
+    *nnz = A.nonZeros();
+    if (!ptr || A.nonZeros() > cap) return;
+    int64_t k = 0;
+    ptr[0] = 0;
+    for (Index i = 0; i < A.rows(); ++i) {
+      for (CsrMatrix::InnerIterator it(A, i); it; ++it) {
+        idx[k] = it.col();
+        val[k] = it.value();
+        ++k;
+      }
+      ptr[i + 1] = k;
+    }
+  });
+}
+
+// GMRES(20) with A = apply_A and M = SEMFEM-AMG on b (caller's), x0 = 0.
+int ref_semfem_solve(double eps, int E, int p, const double* b, double tol, double* x, int* iters, double* rel_res) {
+  return guard([&] {
+    HexMesh m = mesh_of(eps, E, p);
+    SemSpace s(m, p);
+    SemfemPreconditioner pc(s, SemfemInner::Amg);
+    LinOp A = [&s](const FieldVector& in, FieldVector& out) { out = s.apply_A(in); };
+    LinOp M = pc.as_linop();
+    FieldVector bv = Eigen::Map<const Eigen::MatrixXd>(b, s.n(), 1);
+    FieldVector xv = FieldVector::Zero(s.n());
+    GmresConfig cfg;
+    cfg.tol = tol;
+    const GmresStats st = gmres_solve(A, M, bv, xv, cfg);
+    std::memcpy(x, xv.data(), sizeof(double) * size_t(s.n()));
     *iters = st.iterations;
     *rel_res = st.rel_residual;
   });

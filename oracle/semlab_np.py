@@ -1196,3 +1196,70 @@ class Pmg:
         x = self._smooth(l, b, np.zeros_like(b))
         x += self.transfers[l].prolong(self._additive(self.transfers[l].restrict(b), l + 1))
         return x
+
+
+def assemble_semfem(space: SemSpace):
+    """Linear-tetrahedral stiffness on the GLL lattice — semfem.cpp:12-98: every hex sub-cell is
+    covered by its 8 corner tetrahedra with an overall 1/2; masked dofs eliminated (unit
+    diagonal); exact zeros pruned. Vectorised over sub-cells (numpy rounding, not bitwise)."""
+    import scipy.sparse as sps
+    p, E = space.order, space.E
+    X = space.coords
+    Nx, Ny, Nz = space.npts
+    ex, ey, ez = space.mesh.element_ijk()
+    r = np.arange(p)
+    # sub-cell origin lattice indices, element-major then (k, j, i)
+    gx = (ex[:, None, None, None] * p + r[None, None, None, :])
+    gy = (ey[:, None, None, None] * p + r[None, None, :, None])
+    gz = (ez[:, None, None, None] * p + r[None, :, None, None])
+    gx, gy, gz = np.broadcast_arrays(gx, gy, gz)
+    gx, gy, gz = gx.ravel(), gy.ravel(), gz.ravel()
+    cell = np.stack([(gx + cx) + Nx * ((gy + cy) + Ny * (gz + cz))
+                     for cz in (0, 1) for cy in (0, 1) for cx in (0, 1)], axis=1)
+    tets = []
+    for cz in (0, 1):
+        for cy in (0, 1):
+            for cx in (0, 1):
+                c = lambda x, y, z: x + 2 * y + 4 * z  # noqa: E731
+                t = [c(cx, cy, cz), c(1 - cx, cy, cz), c(cx, 1 - cy, cz), c(cx, cy, 1 - cz)]
+                if (cx + cy + cz) % 2:
+                    t[1], t[2] = t[2], t[1]
+                tets.append(t)
+    masked = space.masked.astype(bool)
+    rows, cols, vals = [], [], []
+    for t in tets:
+        v = cell[:, t]
+        P0 = X[v[:, 0]]
+        T = np.stack([X[v[:, 1]] - P0, X[v[:, 2]] - P0, X[v[:, 3]] - P0], axis=2)
+        det = np.linalg.det(T)
+        if np.any(det <= 0.0):
+            raise RuntimeError("assemble_semfem: inverted tetrahedron")
+        Ti = np.linalg.inv(T)
+        grad = np.stack([-Ti.sum(axis=1), Ti[:, 0, :], Ti[:, 1, :], Ti[:, 2, :]], axis=1)
+        K = 0.5 * (det / 6.0)[:, None, None] * np.einsum("nad,nbd->nab", grad, grad)
+        ga = np.broadcast_to(v[:, :, None], K.shape)
+        gb = np.broadcast_to(v[:, None, :], K.shape)
+        keep = ~(masked[ga] | masked[gb])
+        rows.append(ga[keep])
+        cols.append(gb[keep])
+        vals.append(K[keep])
+    mi = np.flatnonzero(masked)
+    rows.append(mi)
+    cols.append(mi)
+    vals.append(np.ones(mi.size))
+    A = sps.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                       shape=(space.n, space.n)).tocsr()
+    A.eliminate_zeros()
+    return A
+
+
+class SemfemPreconditioner:
+    """semfem.cpp:112-134 with the AMG inner solve: z = mask(AmgHierarchy(A_F).vcycle(r))."""
+
+    def __init__(self, space: SemSpace, amg_opts=None):
+        self.space = space
+        self.A = assemble_semfem(space)
+        self.amg = AmgHierarchy(self.A, amg_opts)
+
+    def apply(self, r):
+        return self.space.mask_inplace(self.amg.vcycle(np.asarray(r, dtype=np.float64)))

@@ -115,6 +115,11 @@ SIGNATURES = {
     "semlab_pmg_coarse_info": (i32, [p, pi32, pi64, i32]),
     "semlab_pmg_prolong": (i32, [p, i32, p, p]),
     "semlab_pmg_restrict": (i32, [p, i32, p, p]),
+    "semlab_semfem_create": (i32, [p, C.POINTER(p)]),
+    "semlab_semfem_destroy": (i32, [p]),
+    "semlab_semfem_apply": (i32, [p, p, p]),
+    "semlab_semfem_levels": (i32, [p, pi32, pi64, i32]),
+    "semlab_op_semfem": (i32, [p, C.POINTER(p)]),
     "semlab_gmres_solve": (i32, [p, p, p, p, C.POINTER(GmresConfigC), C.POINTER(GmresStatsC)]),
     "semlab_pcg_solve": (i32, [p, p, p, p, C.POINTER(GmresConfigC), C.POINTER(GmresStatsC)]),
     "semlab_proj_create": (i32, [p, i64, i32, C.POINTER(p)]),

@@ -85,14 +85,17 @@ struct semlab_space_s {
 
 struct semlab_schwarz_s;
 struct semlab_pmg_s;
+struct semlab_semfem_s;
+void semfem_apply(semlab_semfem_s* p, const double* r, double* z);
 
 struct semlab_op_s {
-  enum Kind { kA, kJacobi, kSchwarz, kPmg, kCallback } kind = kA;
+  enum Kind { kA, kJacobi, kSchwarz, kPmg, kCallback, kSemfem } kind = kA;
   semlab_ctx ctx = nullptr;
   int64_t n = 0;
   semlab_space space = nullptr;
   semlab_schwarz_s* sch = nullptr;
   semlab_pmg_s* pmg = nullptr;
+  semlab_semfem_s* semfem = nullptr;
   semlab_apply_fn fn = nullptr;
   void* user = nullptr;
   bool geom32 = false;  // kA: apply with the FP32-rounded geometric factors (smoother operator)

@@ -297,6 +297,32 @@ std::vector<AmgLevelHost> amg_build(const HostCsr& A0, double theta, int max_lev
   return levels;
 }
 
+// Inverse of a dense SPD matrix (host column-major M) into a device buffer: cuSOLVER Cholesky
+// (potrf) and a solve against the identity (potrs). Returns the factorization's info (0 = ok).
+int device_spd_inverse(semlab_ctx ctx, int64_t n, const std::vector<double>& M, DevBuf<double>& inv) {
+  cudaStream_t s = ctx->stream;
+  std::vector<double> I(size_t(n) * n, 0.0);
+  for (int64_t i = 0; i < n; ++i) I[size_t(i) + size_t(n) * i] = 1.0;
+  DevBuf<double> dM(M.size());
+  inv.alloc(I.size());
+  dM.upload(M.data(), M.size(), s);
+  inv.upload(I.data(), I.size(), s);
+  cusolverDnHandle_t h;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(kCuda, "cusolverDnCreate failed");
+  cusolverDnSetStream(h, s);
+  int lwork = 0;
+  cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, int(n), dM.p, int(n), &lwork);
+  DevBuf<double> work(size_t(std::max(lwork, 1)));
+  DevBuf<int> info(1);
+  cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, int(n), dM.p, int(n), work.p, lwork, info.p);
+  cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, int(n), int(n), dM.p, int(n), inv.p, int(n), info.p);
+  int hinfo = 0;
+  SB_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ctx->sync();
+  cusolverDnDestroy(h);
+  return hinfo;
+}
+
 bool dense_spd_inverse(int64_t n, std::vector<double>& M) {
   // Cholesky M = L L^T (lower, column-major), then inverse by solving for the identity.
   std::vector<double> L(M);
@@ -344,35 +370,17 @@ void CoarseSolver::build(semlab_space space, int m) {
     if (nfree > 20000)
       invalid("coarse direct solve is limited to 20000 free dofs (got " + std::to_string(nfree) +
               "); use SEMLAB_COARSE_AMG");
-    std::vector<double> M(size_t(nfree) * nfree, 0.0), I(size_t(nfree) * nfree, 0.0);
-    for (int64_t i = 0; i < nfree; ++i) {
+    std::vector<double> M(size_t(nfree) * nfree, 0.0);
+    for (int64_t i = 0; i < nfree; ++i)
       for (int64_t k = A.ptr[size_t(i)]; k < A.ptr[size_t(i) + 1]; ++k) M[size_t(i) + size_t(nfree) * A.idx[size_t(k)]] = A.val[size_t(k)];
-      I[size_t(i) + size_t(nfree) * i] = 1.0;
-    }
     // Neumann: A has the constants as its nullspace. A + 1 1^T / n is SPD and,
     // on zero-mean right-hand sides, has the zero-mean solution of A e = r.
     if (neumann)
       for (auto& v : M) v += 1.0 / double(nfree);
-    DevBuf<double> dM(M.size());
-    Minv.alloc(I.size());
-    dM.upload(M.data(), M.size(), s);
-    Minv.upload(I.data(), I.size(), s);
-    cusolverDnHandle_t h;
-    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(kCuda, "cusolverDnCreate failed");
-    cusolverDnSetStream(h, s);
-    int lwork = 0;
-    cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, int(nfree), dM.p, int(nfree), &lwork);
-    DevBuf<double> work(size_t(std::max(lwork, 1)));
-    DevBuf<int> info(1);
-    cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, int(nfree), dM.p, int(nfree), work.p, lwork, info.p);
-    cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, int(nfree), int(nfree), dM.p, int(nfree), Minv.p, int(nfree), info.p);
-    int hinfo = 0;
-    SB_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    sp->ctx->sync();
-    cusolverDnDestroy(h);
+    const int hinfo = device_spd_inverse(sp->ctx, nfree, M, Minv);
     if (hinfo != 0) numeric("coarse solve: factorization failed (info " + std::to_string(hinfo) + ")");
     if (neumann) {  // e = Pi M^-1 Pi r with Pi = I - 1 1^T / n: the mean of e is 0
-      std::vector<double> H(I.size());
+      std::vector<double> H(M.size());
       Minv.download(H.data(), H.size(), s);
       sp->ctx->sync();
       const int64_t nn = nfree;
@@ -393,7 +401,20 @@ void CoarseSolver::build(semlab_space space, int m) {
     }
     return;
   }
-  // AMG (amg.cpp:69-129): host setup, device V-cycle
+  build_amg(space, A);
+}
+
+// AMG (amg.cpp:69-129) of a host matrix: host setup, device V-cycle; the coarsest level's dense
+// LDLT (amg.cpp:124-126) becomes a dense inverse (cuSOLVER) applied by one symmetric GEMV.
+void CoarseSolver::build_amg(semlab_space space, const HostCsr& A) {
+  sp = space;
+  mode = SEMLAB_COARSE_AMG;
+  nfree = A.n;
+  cudaStream_t s = sp->ctx->stream;
+  if (rf.n < size_t(nfree)) {
+    rf.alloc(size_t(nfree));
+    zf.alloc(size_t(nfree));
+  }
   auto hl = amg_build(A);
   lev.resize(hl.size());
   for (size_t l = 0; l < hl.size(); ++l) {
@@ -429,14 +450,15 @@ void CoarseSolver::build(semlab_space space, int m) {
   }
   const HostCsr& Ac = hl.back().A;
   coarse_n = Ac.n;
+  if (coarse_n > 20000)  // the reference factors it densely (amg.cpp:124-126): infeasible beyond this
+    numeric("AmgHierarchy: coarsest level has " + std::to_string(coarse_n) +
+            " rows (aggregation stalled); too large for the dense coarse solve");
   std::vector<double> M(size_t(coarse_n) * coarse_n, 0.0);
   for (int64_t i = 0; i < coarse_n; ++i)
     for (int64_t k = Ac.ptr[size_t(i)]; k < Ac.ptr[size_t(i) + 1]; ++k)
       M[size_t(i) + size_t(coarse_n) * Ac.idx[size_t(k)]] = Ac.val[size_t(k)];
-  if (!dense_spd_inverse(coarse_n, M)) numeric("AmgHierarchy: coarse factorization failed");
-  coarse_inv.alloc(M.size());
-  coarse_inv.upload(M.data(), M.size(), s);
-  sp->ctx->sync();
+  if (device_spd_inverse(sp->ctx, coarse_n, M, coarse_inv) != 0) numeric("AmgHierarchy: coarse factorization failed");
+  (void)s;
 }
 
 // AmgHierarchy::cycle (amg.cpp:140-160) with pre = post = 1 damped-Jacobi sweeps.

@@ -36,6 +36,7 @@ std::vector<AmgLevelHost> amg_build(const HostCsr& A, double theta = 0.25, int m
 std::vector<int> amg_aggregate(const HostCsr& A, double theta, int& n_agg);
 // Dense SPD inverse (Cholesky), column-major; false if not positive definite.
 bool dense_spd_inverse(int64_t n, std::vector<double>& M);
+int device_spd_inverse(semlab_ctx ctx, int64_t n, const std::vector<double>& M, DevBuf<double>& inv);
 
 struct CoarseSolver {
   semlab_space sp = nullptr;
@@ -58,6 +59,7 @@ struct CoarseSolver {
   DevBuf<double> gsend, grecv, rfull, zfull;  // distributed gather of the coarse residual
   bool neumann = false;  // singular coarse problem: solve on the zero-mean subspace
   void build(semlab_space space, int mode);
+  void build_amg(semlab_space space, const HostCsr& A);  // AMG hierarchy of a given matrix
   void solve(const double* r_full, double* z_full);
   void solve_dist(semlab_space dist_space, const double* r_loc, double* z_loc);
   void amg_cycle(int l, const double* r, double* z);

@@ -310,6 +310,7 @@ void semlab_op_s::apply(const double* in, double* out) {
     case kJacobi: ctx->count(launch_mul(out, space->jacobi_inv(), in, n, ctx->stream)); break;
     case kSchwarz: sch->apply(in, out); break;
     case kPmg: pmg->vcycle(in, out); break;
+    case kSemfem: semfem_apply(semfem, in, out); break;
     case kCallback: fn(user, in, out); break;
     default: invalid("semlab_op: operator kind not available");
   }

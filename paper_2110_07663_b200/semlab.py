@@ -484,6 +484,38 @@ class _BorrowedSpace(SemSpace):
         pass
 
 
+class SemfemPreconditioner:
+    """SemfemPreconditioner(space, SemfemInner::Amg), semfem.hpp:36-54: the linear-tetrahedral
+    stiffness matrix on the space's GLL lattice with one AMG V-cycle as the inner solve."""
+
+    def __init__(self, space: SemSpace):
+        self.space = space
+        h = C.c_void_p()
+        check(lib.semlab_semfem_create(space.handle, C.byref(h)))
+        self.handle = h
+        _own(self, h, lib.semlab_semfem_destroy, space)
+
+    def apply(self, r, out: torch.Tensor | None = None) -> torch.Tensor:
+        r = self.space.to_device(r)
+        out = self.space.zeros() if out is None else out
+        check(lib.semlab_semfem_apply(self.handle, _ptr(r), _ptr(out)))
+        return out
+
+    def levels(self) -> list:
+        nl = C.c_int()
+        sizes = (C.c_int64 * 64)()
+        check(lib.semlab_semfem_levels(self.handle, C.byref(nl), sizes, 64))
+        return [int(sizes[i]) for i in range(nl.value)]
+
+    def as_linop(self) -> LinOp:
+        h = C.c_void_p()
+        check(lib.semlab_op_semfem(self.handle, C.byref(h)))
+        return LinOp(h, self.space.n, self.space.ctx, keep=self)
+
+    def __del__(self):
+        _release(self)
+
+
 @dataclass
 class GmresConfig:
     restart: int = 20

@@ -11,6 +11,8 @@ import pytest
 from oracle import semlab_np as o
 
 G = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_golden.npz"))
+REF_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "libsemlab_ref.so")
 OP_CASES = [(1.0, 2, 2), (0.3, 2, 3), (0.3, 2, 4), (1.0, 4, 7), (0.3, 4, 7)]
 
 
@@ -135,3 +137,25 @@ def test_pmg_variants_pinned(name):
     z = pmg.vcycle(g[f"vc_{name}_b"])
     want = g[f"vc_{name}_z"]
     assert np.abs(z - want).max() <= 1e-10 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("eps,E,p", [(0.3, 2, 3), (1.0, 2, 5), (0.05, 2, 4)])
+def test_semfem_matrix_pinned(eps, E, p):
+    """assemble_semfem (semfem.cpp:12-98) restated in numpy against the reference's own matrix."""
+    import ctypes as C
+    if not os.path.exists(REF_LIB):
+        pytest.skip("oracle/_ref not built")
+    lib = C.CDLL(REF_LIB)
+    nnz = C.c_int64()
+    assert lib.ref_semfem_matrix(C.c_double(eps), E, p, C.byref(nnz), None, None, None, C.c_int64(0)) == 0
+    n = (E * p + 1) ** 3
+    ptr, idx, val = np.zeros(n + 1, np.int64), np.zeros(nnz.value, np.int64), np.zeros(nnz.value)
+    pi64 = C.POINTER(C.c_int64)
+    assert lib.ref_semfem_matrix(C.c_double(eps), E, p, C.byref(nnz), ptr.ctypes.data_as(pi64),
+                                 idx.ctypes.data_as(pi64), val.ctypes.data_as(C.POINTER(C.c_double)),
+                                 C.c_int64(nnz.value)) == 0
+    import scipy.sparse as sps
+    ref = sps.csr_matrix((val, idx, ptr), shape=(n, n))
+    got = o.assemble_semfem(o.SemSpace(o.generate_kershaw(eps, E), p))
+    d = abs(got - ref)  # entries present in only one matrix (cancellation to an exact 0 in one
+    assert d.max() <= 1e-13 * abs(ref).max()  # summation order) are roundoff-sized: covered here
