@@ -33,6 +33,13 @@ struct Error : std::runtime_error {
                                   __FILE__ + ":" + std::to_string(__LINE__) + ")");        \
   } while (0)
 
+// NCCL status -> sb::Error (kNccl); needs <nccl.h> in the including translation unit.
+#define SB_NCCL(call)                                                                  \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess) ::sb::fail(::sb::kNccl, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
 // Check the last launch (launch-configuration errors surface immediately; asynchronous
 // faults surface at the next synchronising call).
 #define SB_LAUNCH_CHECK() SB_CUDA(cudaGetLastError())

@@ -732,13 +732,18 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 3 : 1) k_asm_boxes(const
   }
 }
 
-// out[g] = (1/count) * sum over elements whose participating box covers g, ascending id
+// out[g] = (1/count) * sum over elements whose participating box covers g, ascending id.
+// On a z-slab the sum also covers the ghost planes, and on the exchange planes (zb-1, zb, zb+1
+// below an internal boundary; zt-1, zt, zt+1 above one) it writes the raw local sum to out and
+// the local count to cnt[plane][x + Nx y] (planes 0..2 bottom, 3..5 top) for asm_exchange.
 template <int P, class T>
-__global__ void k_asm_sum(const Slab sl, const T* __restrict__ boxes, double* __restrict__ out) {
+__global__ void k_asm_sum(const Slab sl, const T* __restrict__ boxes, double* __restrict__ out,
+                          double* __restrict__ cnt) {
   constexpr int P2 = P * P, P3 = P2 * P;
   const int q = sl.q;
   const bool dir = sl.dirichlet != 0;
-  const int64_t z0 = int64_t(sl.ez0) * q, nz = int64_t(sl.ez1 - sl.ez0) * q + 1;
+  const int64_t zb = int64_t(sl.ez0) * q, zt = int64_t(sl.ez1) * q;
+  const int64_t z0 = zb - sl.nranks_below, nz = zt + sl.nranks_above - z0 + 1;
   const int64_t total = sl.Nx * sl.Ny * nz;
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
     const int64_t x = t % sl.Nx, y = (t / sl.Nx) % sl.Ny, z = z0 + t / (sl.Nx * sl.Ny);
@@ -769,7 +774,26 @@ __global__ void k_asm_sum(const Slab sl, const T* __restrict__ boxes, double* __
           acc += double(boxes[el * P3 + ca[2][k] * P2 + ca[1][j] * P + ca[0][i]]);
           ++count;
         }
-    out[sl.lidx(x, y, z)] = count > 0 ? acc * (1.0 / double(count)) : 0.0;
+    int plane = -1;
+    if (sl.nranks_below && z <= zb + 1) plane = int(z - (zb - 1));
+    if (sl.nranks_above && z >= zt - 1) plane = 3 + int(z - (zt - 1));
+    if (plane >= 0) {
+      out[sl.lidx(x, y, z)] = acc;
+      cnt[int64_t(plane) * sl.Nx * sl.Ny + x + sl.Nx * y] = double(count);
+    } else {
+      out[sl.lidx(x, y, z)] = count > 0 ? acc * (1.0 / double(count)) : 0.0;
+    }
+  }
+}
+
+// ASM on slabs, after the exchange: plane = lower partial + upper partial over the summed counts
+// (both ranks form the interface plane in the same order: bitwise identical copies).
+__global__ void k_asm_combine(double* __restrict__ v, const double* __restrict__ lo_sum,
+                              const double* __restrict__ lo_cnt, const double* __restrict__ hi_sum,
+                              const double* __restrict__ hi_cnt, int64_t P) {
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < P; t += int64_t(gridDim.x) * blockDim.x) {
+    const double c = lo_cnt[t] + hi_cnt[t];
+    v[t] = c > 0.0 ? (lo_sum[t] + hi_sum[t]) * (1.0 / c) : 0.0;
   }
 }
 
@@ -841,14 +865,15 @@ struct Launch {
     }
   }
   template <int P>
-  static void asm_(const Slab& sl, const T* S, const T* L, const double* r, void* boxes, double* out, cudaStream_t s) {
+  static void asm_(const Slab& sl, const T* S, const T* L, const double* r, void* boxes, double* out, double* cnt,
+                   cudaStream_t s) {
     using Sh = Shape<P, T>;
     const int grid = int((sl.elems() + Sh::EPC - 1) / Sh::EPC);
     prep(k_asm_boxes<P, T>, Sh::smem());
     k_asm_boxes<P, T><<<grid, Sh::NT, Sh::smem(), s>>>(sl, S, L, r, static_cast<T*>(boxes));
-    const int64_t total = sl.Nx * sl.Ny * (int64_t(sl.ez1 - sl.ez0) * sl.q + 1);
+    const int64_t total = sl.Nx * sl.Ny * (int64_t(sl.ez1 - sl.ez0) * sl.q + 1 + sl.nranks_below + sl.nranks_above);
     k_asm_sum<P, T><<<int(std::min<int64_t>((total + 255) / 256, 148 * 32)), 256, 0, s>>>(
-        sl, static_cast<const T*>(boxes), out);
+        sl, static_cast<const T*>(boxes), out, cnt);
   }
   template <int P>
   static void boxes(const Slab& sl, const T* S, const T* L, const double* in, double* out, cudaStream_t s) {
@@ -892,15 +917,15 @@ int64_t launch_ras(const Slab& sl, int precision, const void* S, const void* L, 
 }
 
 int64_t launch_asm(const Slab& sl, int precision, const void* S, const void* L, const double* r, void* boxes,
-                   double* out, cudaStream_t s) {
+                   double* out, double* cnt, cudaStream_t s) {
   if (sl.elems() == 0) return 0;
   const int P = sl.q + 3;
   if (precision == 32) {
-#define C32(PP) Launch<float>::asm_<PP>(sl, static_cast<const float*>(S), static_cast<const float*>(L), r, boxes, out, s)
+#define C32(PP) Launch<float>::asm_<PP>(sl, static_cast<const float*>(S), static_cast<const float*>(L), r, boxes, out, cnt, s)
     SB_FDM_SWITCH(P, C32)
 #undef C32
   } else {
-#define C64(PP) Launch<double>::asm_<PP>(sl, static_cast<const double*>(S), static_cast<const double*>(L), r, boxes, out, s)
+#define C64(PP) Launch<double>::asm_<PP>(sl, static_cast<const double*>(S), static_cast<const double*>(L), r, boxes, out, cnt, s)
     SB_FDM_SWITCH(P, C64)
 #undef C64
   }
@@ -921,6 +946,13 @@ int64_t launch_fdm_boxes(const Slab& sl, int precision, const void* S, const voi
     SB_FDM_SWITCH(P, C64)
 #undef C64
   }
+  SB_LAUNCH_CHECK();
+  return 1;
+}
+
+int64_t launch_asm_combine(double* v, const double* lo_sum, const double* lo_cnt, const double* hi_sum,
+                           const double* hi_cnt, int64_t P, cudaStream_t s) {
+  k_asm_combine<<<int(std::min<int64_t>((P + 255) / 256, 148 * 8)), 256, 0, s>>>(v, lo_sum, lo_cnt, hi_sum, hi_cnt, P);
   SB_LAUNCH_CHECK();
   return 1;
 }

@@ -1,3 +1,4 @@
+#include <nccl.h>
 // SchwarzSmoother: host setup restated from schwarz.cpp:46-214 (box lengths, extended 1-D
 // operators, generalised eigendecomposition), device apply in k_fdm.cu.
 #include "schwarz.hpp"
@@ -179,7 +180,8 @@ void semlab_schwarz_s::apply(const double* r, double* z) {
   semlab_space_s& sp = *space;
   SB_CUDA(cudaMemsetAsync(z, 0, size_t(sp.n) * sizeof(double), sp.ctx->stream));
   if (sp.distributed()) {
-    if (mode != SEMLAB_SCHWARZ_RAS) invalid("SchwarzSmoother: ASM is not available on a distributed space (use RAS)");
+    if (mode == SEMLAB_SCHWARZ_ASM && sp.sl.q < 3 && sp.sl.ez1 - sp.sl.ez0 < 2)
+      invalid("SchwarzSmoother: ASM on slabs needs order >= 3 or >= 2 element layers per rank");
     // the ghost planes of a slab vector are scratch: fill them with the neighbours' planes
     sp.halo_exchange(const_cast<double*>(r));
   }
@@ -189,7 +191,58 @@ void semlab_schwarz_s::apply(const double* r, double* z) {
     ras(r, 0, e);
     sp.owner_copy_up(z);
   } else {
-    sp.ctx->count(launch_asm(sp.sl, precision, S.p, L.p, r, boxes.p, z, sp.ctx->stream));
+    const int64_t P2 = sp.sl.Nx * sp.sl.Ny;
+    if (cnt.n < size_t(6 * P2)) cnt.alloc(size_t(6 * P2));
+    sp.ctx->count(launch_asm(sp.sl, precision, S.p, L.p, r, boxes.p, z, cnt.p, sp.ctx->stream));
+    if (sp.distributed()) asm_exchange(z);
+  }
+}
+
+// ASM on z-slabs (schwarz.cpp:269-287 across ranks): the boxes of an element layer next to an
+// internal boundary reach one lattice plane into the neighbour slab, so the neighbour's boxes add
+// to this rank's planes zb, zb+1 (from below) and zt-1, zt (from above). Each rank sends its raw
+// sums and counts on the planes its boxes share with a neighbour (zb-1, zb down; zt, zt+1 up),
+// receives the neighbour's, and forms (lower sum + upper sum) / (lower count + upper count), the
+// lower rank's (lower element ids) partial first; the ghost planes are zeroed.
+void semlab_schwarz_s::asm_exchange(double* z) {
+  semlab_space_s& sp = *space;
+  const Slab& sl = sp.sl;
+  const int64_t P2 = sl.Nx * sl.Ny;
+  if (xch.n < size_t(8 * P2)) xch.alloc(size_t(8 * P2));
+  ncclComm_t comm = static_cast<ncclComm_t>(sp.ctx->nccl);
+  cudaStream_t s = sp.ctx->stream;
+  const int r = sp.ctx->rank;
+  const int64_t zb = int64_t(sl.ez0) * sl.q, zt = int64_t(sl.ez1) * sl.q;
+  auto plane = [&](int64_t zz) { return z + sl.lidx(0, 0, zz); };
+  auto cplane = [&](int k) { return cnt.p + k * P2; };
+  auto rplane = [&](int k) { return xch.p + k * P2; };  // 0..3 from below, 4..7 from above
+  SB_NCCL(ncclGroupStart());
+  if (sl.nranks_below) {  // my (zb-1, zb) -> its (zt'-1, zt'); its (zt', zt'+1) -> my (zb, zb+1)
+    SB_NCCL(ncclSend(plane(zb - 1), size_t(P2), ncclDouble, r - 1, comm, s));
+    SB_NCCL(ncclSend(plane(zb), size_t(P2), ncclDouble, r - 1, comm, s));
+    SB_NCCL(ncclSend(cplane(0), size_t(P2), ncclDouble, r - 1, comm, s));
+    SB_NCCL(ncclSend(cplane(1), size_t(P2), ncclDouble, r - 1, comm, s));
+    for (int k = 0; k < 4; ++k) SB_NCCL(ncclRecv(rplane(k), size_t(P2), ncclDouble, r - 1, comm, s));
+  }
+  if (sl.nranks_above) {  // my (zt, zt+1) -> its (zb', zb'+1); its (zb'-1, zb') -> my (zt-1, zt)
+    SB_NCCL(ncclSend(plane(zt), size_t(P2), ncclDouble, r + 1, comm, s));
+    SB_NCCL(ncclSend(plane(zt + 1), size_t(P2), ncclDouble, r + 1, comm, s));
+    SB_NCCL(ncclSend(cplane(4), size_t(P2), ncclDouble, r + 1, comm, s));
+    SB_NCCL(ncclSend(cplane(5), size_t(P2), ncclDouble, r + 1, comm, s));
+    for (int k = 0; k < 4; ++k) SB_NCCL(ncclRecv(rplane(4 + k), size_t(P2), ncclDouble, r + 1, comm, s));
+  }
+  SB_NCCL(ncclGroupEnd());
+  // from below the order is (sum zt', sum zt'+1, cnt zt', cnt zt'+1) = my (zb, zb+1)
+  if (sl.nranks_below) {
+    sp.ctx->count(launch_asm_combine(plane(zb), rplane(0), rplane(2), plane(zb), cplane(1), P2, s));
+    sp.ctx->count(launch_asm_combine(plane(zb + 1), rplane(1), rplane(3), plane(zb + 1), cplane(2), P2, s));
+    SB_CUDA(cudaMemsetAsync(plane(zb - 1), 0, size_t(P2) * sizeof(double), s));
+  }
+  // from above: (sum zb'-1, sum zb', cnt zb'-1, cnt zb') = my (zt-1, zt); mine first (lower ids)
+  if (sl.nranks_above) {
+    sp.ctx->count(launch_asm_combine(plane(zt - 1), plane(zt - 1), cplane(3), rplane(4), rplane(6), P2, s));
+    sp.ctx->count(launch_asm_combine(plane(zt), plane(zt), cplane(4), rplane(5), rplane(7), P2, s));
+    SB_CUDA(cudaMemsetAsync(plane(zt + 1), 0, size_t(P2) * sizeof(double), s));
   }
 }
 

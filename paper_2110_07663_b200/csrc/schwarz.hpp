@@ -10,6 +10,8 @@ struct semlab_schwarz_s {
   int precision = 32;
   int P = 0;
   sb::DevBuf<unsigned char> S, L, boxes;
+  sb::DevBuf<double> cnt, xch;  // ASM on slabs: local counts (6 planes) and received sums/counts (8 planes)
+  void asm_exchange(double* z);
   std::vector<double> hlen;  // 3 per local element
   std::vector<double> hlam;  // 3*P per local element (padded with 1)
   std::vector<int> hn;       // 3 per local element

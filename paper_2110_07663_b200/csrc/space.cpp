@@ -13,11 +13,6 @@
 
 using namespace sb;
 
-#define SB_NCCL(call)                                                                  \
-  do {                                                                                 \
-    ncclResult_t r_ = (call);                                                          \
-    if (r_ != ncclSuccess) fail(kNccl, std::string(#call) + ": " + ncclGetErrorString(r_)); \
-  } while (0)
 
 // ------------------------------------------------------------------------------ context
 void semlab_ctx_s::allreduce_device(double* d_vals, int K) {

@@ -69,8 +69,12 @@ def main():
     r = c.mask_inplace(np.random.default_rng(1).standard_normal(c.n))
     out["ras64"] = rel(gather(sch.apply(r[sl.local_slice()])), so.apply(r))
 
+    out["asm64"] = rel(gather(S.SchwarzSmoother(sp, S.ASM, 64).apply(r[sl.local_slice()])),
+                       o.SchwarzSmoother(c, o.ASM, 64).apply(r))
+    out["ras32"] = rel(gather(S.SchwarzSmoother(sp, S.RAS, 32).apply(r[sl.local_slice()])),
+                       o.SchwarzSmoother(c, o.RAS, 32).apply(r))
     # Neumann mode over z-slabs: global mean removal (sem_space.cpp:207), unmasked diagonal,
-    # RAS with Neumann faces (schwarz.cpp:151-160; ASM is single-GPU only)
+    # RAS/ASM with Neumann faces (schwarz.cpp:151-160)
     spn = S.SemSpace(mesh, p, S.NEUMANN)
     cn = o.SemSpace(o.generate_kershaw(eps, E), p, o.NEUMANN)
     out["ax_neumann"] = rel(gather(spn.apply_A(u[sl.local_slice()])), cn.apply_A(u))
@@ -78,6 +82,8 @@ def main():
     rn = np.random.default_rng(2).standard_normal(c.n)
     out["ras64_neumann"] = rel(gather(S.SchwarzSmoother(spn, S.RAS, 64).apply(rn[sl.local_slice()])),
                                o.SchwarzSmoother(cn, o.RAS, 64).apply(rn))
+    out["asm64_neumann"] = rel(gather(S.SchwarzSmoother(spn, S.ASM, 64).apply(rn[sl.local_slice()])),
+                               o.SchwarzSmoother(cn, o.ASM, 64).apply(rn))
     # ProjectionBasis (krylov.cpp:131-152) with rank-local owned-range reductions
     X = np.random.default_rng(3).standard_normal((3, c.n))
     pbg, pbo = S.ProjectionBasis(2), o.ProjectionBasis(2)
@@ -113,6 +119,12 @@ def main():
     out["vcycle_jac_31"] = rel(np.concatenate(_allg(z3.cpu().numpy()[s3.owned_slice_local()], world)), pmjo.vcycle(b3))
     out["vcycle"] = rel(gather(pm.vcycle(b_loc)), pmo.vcycle(bo))
 
+    # Chebyshev-ASM hierarchy on slabs (generic Chebyshev path with the ASM exchange)
+    pma = S.Pmg(mesh, (7, 3, 1), S.ASM_SMOOTHER, 2, 0.1, 1.1, 64, S.COARSE_DIRECT)
+    pmao = o.Pmg(o.generate_kershaw(eps, E), (7, 3, 1), "asm", 2, 0.1, 1.1, "direct", 64)
+    out["vcycle_asm"] = rel(gather(pma.vcycle(b_loc)), pmao.vcycle(bo))
+    del pma
+
     x = torch.zeros_like(b_loc)
     st = S.gmres_solve(pm.spaces[0].as_linop(), pm.as_linop(), b_loc, x, S.GmresConfig())
     xo = np.zeros(c.n)
@@ -120,6 +132,16 @@ def main():
     out["gmres_iters"] = [st.iterations, sto.iterations]
     out["gmres_conv"] = bool(st.converged)
     out["gmres_x"] = rel(gather(x), xo)
+    # the bench setting on slabs: FP32 smoother (fused slab Chebyshev-RAS, FP32-factor Ax), FP64 GMRES
+    pm32 = S.Pmg(mesh, (7, 3, 1), S.RAS_SMOOTHER, 2, 0.1, 1.1, 32, S.COARSE_AMG)
+    pmo_amg = o.Pmg(o.generate_kershaw(eps, E), (7, 3, 1), "ras", 2, 0.1, 1.1, "amg", 64)
+    x32 = torch.zeros_like(b_loc)
+    st32 = S.gmres_solve(pm32.spaces[0].as_linop(), pm32.as_linop(), b_loc, x32, S.GmresConfig())
+    xa = np.zeros(c.n)
+    sta = o.gmres_solve(c.apply_A, pmo_amg.vcycle, bo, xa, o.GmresConfig())
+    out["gmres32_iters"] = [st32.iterations, sta.iterations]
+    out["gmres32_conv"] = bool(st32.converged)
+    out["gmres32_x"] = rel(gather(x32), xa)
     if rank == 0:
         print("DIST_RESULT " + json.dumps(out), flush=True)
     dist.barrier()

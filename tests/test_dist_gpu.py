@@ -16,11 +16,12 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
-def test_distributed_matches_oracle(nproc):
+@pytest.mark.parametrize("nproc,E", [(2, 4), (4, 4), (2, 8), (4, 8)])
+def test_distributed_matches_oracle(nproc, E):
+    """E=4: one or two element layers per rank; E=8: two or four."""
     if _ngpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    env = dict(os.environ, DIST_E="4", DIST_EPS="0.3")
+    env = dict(os.environ, DIST_E=str(E), DIST_EPS="0.3")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "dist_worker.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
@@ -31,6 +32,11 @@ def test_distributed_matches_oracle(nproc):
     assert r["dot"] < 1e-12
     assert r["mass"] < 1e-13 and r["diag"] < 1e-12
     assert r["ras64"] < 1e-12
+    assert r["asm64"] < 1e-12 and r["asm64_neumann"] < 1e-12, r
+    assert r["ras32"] < 2e-6, r
+    assert r["vcycle_asm"] < 1e-10, r
+    it32, ito32 = r["gmres32_iters"]
+    assert r["gmres32_conv"] and abs(it32 - ito32) <= 1 and r["gmres32_x"] < 1e-6, r
     assert r["ax_neumann"] < 1e-12 and r["diag_neumann"] < 1e-12, r
     assert r["ras64_neumann"] < 1e-12, r
     assert r["proj"] < 1e-11, r
