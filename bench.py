@@ -113,7 +113,8 @@ REF_MAX_ITERS = 6
 def ref_bench_cmd(cfg, iters, warm):
     return [REF_BENCH, "--eps", str(cfg["eps"]), "--elems", str(cfg["E"]), "--order", str(cfg["p"]),
             "--smoother", cfg["smoother"], "--coarse", cfg["coarse"], "--cheb-order", str(cfg["eta"]),
-            "--krylov", cfg["krylov"], "--iters", str(iters), "--warmup-iters", str(warm)]
+            "--krylov", cfg["krylov"], "--iters", str(iters), "--warmup-iters", str(warm),
+            "--pmg", "1" if len(cfg["orders"]) > 1 else "0"]
 
 
 def ref_sample_desc(cfg, r, warm):
@@ -247,7 +248,8 @@ def run_ours(args, cfg, name):
     # the reference on this same workload runs beside the GPU measurement (rank 0, N=1 only)
     cpu_proc = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_proc = start_cpu_reference(cfg, args.cpu_iters, 0)
+        n_est = (cfg["E"] * cfg["p"] + 1) ** 3  # ~1 s of reference iterations at c1-c3, one at c4
+        cpu_proc = start_cpu_reference(cfg, args.cpu_iters or max(1, min(100, int(2e7 / n_est))), 0)
     sm = {"ras": S.RAS_SMOOTHER, "jacobi": S.JACOBI_SMOOTHER, "asm": S.ASM_SMOOTHER}[cfg["smoother"]]
     cm = S.COARSE_AMG if cfg["coarse"] == "amg" else S.COARSE_DIRECT
     t0 = time.time()
@@ -366,6 +368,16 @@ def run_ours(args, cfg, name):
     w = torch.empty_like(u)
     roofs = {}
 
+    def guarded(fn):
+        """A roofline probe that does not fit next to the solve (E = 96^3 on one GPU) is skipped."""
+        try:
+            fn()
+        except (RuntimeError, MemoryError) as ex:
+            skipped.append(f"{getattr(fn, '__name__', 'probe')}: {str(ex)[:120]}")
+            torch.cuda.empty_cache()
+
+    skipped = []
+
     def add(key, kernel, nbytes, t, launches=1, per_solve=None):
         ach = nbytes / t / 1e9
         roofs[key] = {"kernel": kernel, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
@@ -384,7 +396,7 @@ def run_ours(args, cfg, name):
         if cfg["p"] == 7 and cfg["precision"] == 32:
             add("ax32", "k_axw<.,float>: smoother Ax, FP32-rounded factors, FP64 DMMA", kb["ax32"],
                 timed(lambda: sp.apply_A_geom32(u, w)), per_solve=6 * its)
-        if cfg["smoother"] == "ras":
+        def ras_probes():
             sch = S.SchwarzSmoother(sp, S.RAS, cfg["precision"])
             add("ras0", "k_rasw mode 0: RAS, FP32 FDM local solves, owner write", kb["ras0"],
                 timed(lambda: sch.apply(u, w)), per_solve=6 * its)
@@ -404,11 +416,16 @@ def run_ours(args, cfg, name):
                 f"{cfg['eta'] + 1} fused RAS launches (init, step, last)", cheb_bytes, timed(smooth),
                 launches=2 * (cfg["eta"] + 1) + 1, per_solve=2 * its * (2 * (cfg["eta"] + 1) + 1))
             del cheb, sch, xs
+
+        if cfg["smoother"] == "ras":
+            guarded(ras_probes)
         n1 = (cfg["E"] * 3 + 1) ** 3
         tot, vcyc = solve_bytes(cfg, sp.n, E_loc, n1, E_loc, int(round(its)))
         if pmg is not None and cfg["smoother"] == "ras" and cfg["orders"][1:2] == (3,):
-            vt = timed(lambda: pmg.vcycle(b, w), reps=10)
-            add("vcycle", "one pMG V-cycle (all levels, CUDA graph)", vcyc, vt, per_solve=its)
+            def vcycle_probe():
+                vt = timed(lambda: pmg.vcycle(b, w), reps=10)
+                add("vcycle", "one pMG V-cycle (all levels, CUDA graph)", vcyc, vt, per_solve=its)
+            guarded(vcycle_probe)
     if world == 1 and pmg is not None and cfg["smoother"] == "ras" and cfg["orders"][1:2] == (3,):
         solver_roof = {"algorithmic_bytes_per_solve": tot, "t_solve_ms": t_solve_s * 1e3,
                        "achieved": tot / t_solve_s / 1e9, "peak": peak, "unit": "GB/s",
@@ -475,7 +492,8 @@ def run_ours(args, cfg, name):
                            "krylov_precision": "fp64", "parallelism": f"z-slab x{world}", "setup_s": setup_s,
                            "l2": "inputs larger than L2 (geometry 805 MB at E=32^3)",
                            "time_to_1e-8_ms": t / args.steps * 1e3, "step_wall_ms": [round(v, 1) for v in step_ms]},
-                "e2e": e2e, "roofline": dominant, "rooflines": roofs, "solver_roofline": solver_roof,
+                "e2e": e2e, "roofline": dominant, "rooflines": roofs, "rooflines_skipped": skipped or None,
+                "solver_roofline": solver_roof,
                 "fp64_smoother": fp64, "cpu_baseline": cpu, "clocks": clk.summary(),
                 "gpu_launches": launches}
         print(json.dumps(line), flush=True)
@@ -491,8 +509,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=1,
-                    help="iterations of the reference timed for cpu_baseline (after its setup)")
+    ap.add_argument("--cpu-iters", type=int, default=0,
+                    help="iterations of the reference timed for cpu_baseline after its setup (0: sized to the mesh)")
     ap.add_argument("--no-fp64-line", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "ref_ext.hpp"
@@ -24,7 +25,7 @@ using namespace semlab_ref;
 
 int main(int argc, char** argv) {
   double eps = 0.3;
-  int E = 32, p = 7, eta = 2, iters = 20, warm = 1;
+  int E = 32, p = 7, eta = 2, iters = 20, warm = 1, use_pmg = 1;
   std::string smoother = "ras", coarse = "amg", krylov = "gmres";
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
@@ -37,15 +38,26 @@ int main(int argc, char** argv) {
     else if (k == "--krylov") krylov = v;
     else if (k == "--iters") iters = std::stoi(v);
     else if (k == "--warmup-iters") warm = std::stoi(v);
+    else if (k == "--pmg") use_pmg = std::stoi(v);
   }
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   HexMesh m = generate_kershaw(KershawParams{eps, E}, p);
   std::vector<int> orders = p > 3 ? std::vector<int>{p, 3, 1} : std::vector<int>{p, 1};
-  Pmg pmg(m, orders, smoother, eta, 0.1, 1.1, coarse);
-  const SemSpace& s = *pmg.spaces[0];
+  std::unique_ptr<Pmg> pmg;
+  std::unique_ptr<SemSpace> own;
+  FieldVector inv;
+  LinOp M;
+  if (use_pmg) {
+    pmg = std::make_unique<Pmg>(m, orders, smoother, eta, 0.1, 1.1, coarse);
+    M = pmg->as_linop();
+  } else {  // config c1: Jacobi-preconditioned CG, no multigrid
+    own = std::make_unique<SemSpace>(m, p);
+    inv = jacobi_inverse_diag(*own);
+    M = [&inv](const FieldVector& in, FieldVector& out) { out = inv.cwiseProduct(in); };
+  }
+  const SemSpace& s = use_pmg ? *pmg->spaces[0] : *own;
   LinOp A = [&s](const FieldVector& in, FieldVector& out) { out = s.apply_A(in); };
-  LinOp M = pmg.as_linop();
   FieldVector b = build_rhs(s, 1);
   const double t_setup = std::chrono::duration<double>(clk::now() - t0).count();
   auto solve = [&](int k) {

@@ -1014,27 +1014,26 @@ __device__ __forceinline__ void face_node7(const Slab& sl, const double* __restr
   epi(g, acc);
 }
 
-// The slab's face nodes in three launches of 2-D grids (x along the threads, no divisions):
-//   FAM 0: planes z = q k (all x, y)        grid (., Ny, nzl + 1)
-//   FAM 1: z % q != 0, y = q j (all x)      grid (., Ey + 1, nzl (q-1))
-//   FAM 2: z, y % q != 0, x = q i           grid (., Ey, nzl (q-1)), threads over (i, y in the row)
-template <int FAM, class EpiT>
+// One launch for the three families: blockIdx.z enumerates the z planes of the slab
+// (z = zb + zz, zz = 0 .. nzl q); blockIdx.y the rows of the plane's family; x along threads.
+//   z % q == 0 (FAM 0): rows y = 0 .. Ny-1, threads over x
+//   z % q != 0: rows 0 .. Ey  are FAM 1 (y = q row, threads over x);
+//               rows Ey+1 .. 2Ey are FAM 2 (y in element row ey = row-Ey-1, threads over (i, y-1-q ey))
+template <class EpiT>
 __global__ void __launch_bounds__(128) k_face_epi7(const Slab sl, const double* __restrict__ fb, const EpiT epi) {
   constexpr int q = 7;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int zb = sl.ez0 * q;
-  if (FAM == 0) {
+  const int zz = int(blockIdx.z), z = sl.ez0 * q + zz, row = int(blockIdx.y);
+  if (zz % q == 0) {
+    if (t >= sl.Nx || row >= sl.Ny) return;
+    face_node7(sl, fb, epi, t, row, z);
+  } else if (row <= sl.Ey) {
     if (t >= sl.Nx) return;
-    face_node7(sl, fb, epi, t, int(blockIdx.y), zb + int(blockIdx.z) * q);
-  } else if (FAM == 1) {
-    if (t >= sl.Nx) return;
-    const int zz = int(blockIdx.z);
-    face_node7(sl, fb, epi, t, int(blockIdx.y) * q, zb + (zz / (q - 1)) * q + 1 + zz % (q - 1));
-  } else {  // threads over (x-plane i, y inside the element row): t = 6 i + (y - q ey - 1)
+    face_node7(sl, fb, epi, t, row * q, z);
+  } else {
     const int i = t / (q - 1), yi = t - i * (q - 1);
-    if (i > sl.Ex) return;
-    const int zz = int(blockIdx.z);
-    face_node7(sl, fb, epi, i * q, int(blockIdx.y) * q + 1 + yi, zb + (zz / (q - 1)) * q + 1 + zz % (q - 1));
+    if (i > sl.Ex || row > 2 * sl.Ey) return;
+    face_node7(sl, fb, epi, i * q, (row - sl.Ey - 1) * q + 1 + yi, z);
   }
 }
 
@@ -1053,12 +1052,12 @@ int64_t axw_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
   const int grid = capped_grid(std::min<int64_t>(nctas, (nE + W - 1) / W));
   kern<<<grid, 32 * W, smem, s>>>(sl, dmat<8>(sl.q), u, geom, sy.dep, epi);
   SB_LAUNCH_CHECK();
-  const unsigned nzl = unsigned(sl.ez1 - sl.ez0), bx = unsigned((sl.Nx + 127) / 128);
-  k_face_epi7<0><<<dim3(bx, unsigned(sl.Ny), nzl + 1), 128, 0, s>>>(sl, sy.dep, epi);
-  k_face_epi7<1><<<dim3(bx, unsigned(sl.Ey + 1), nzl * 6), 128, 0, s>>>(sl, sy.dep, epi);
-  k_face_epi7<2><<<dim3(unsigned(((sl.Ex + 1) * 6 + 127) / 128), unsigned(sl.Ey), nzl * 6), 128, 0, s>>>(sl, sy.dep, epi);
+  const unsigned nzl = unsigned(sl.ez1 - sl.ez0);
+  const unsigned bx = unsigned((std::max<int64_t>(sl.Nx, (sl.Ex + 1) * 6) + 127) / 128);
+  const unsigned by = unsigned(std::max<int64_t>(sl.Ny, 2 * sl.Ey + 1));
+  k_face_epi7<<<dim3(bx, by, nzl * 7 + 1), 128, 0, s>>>(sl, sy.dep, epi);
   SB_LAUNCH_CHECK();
-  return 4;
+  return 2;
 }
 
 bool ax_dmma() {  // SEMLAB_AX_DMMA=0 selects the FP64-FMA persistent kernel (A/B measurement)

@@ -49,10 +49,13 @@ def _own(obj, handle, destroy, *parents):
 
 def _release(obj):
     box = getattr(obj, "_box", None)
-    if box is not None and box[0]:
-        for child in box[2]:
-            _release_box(child)
-        _release_box(box)
+    try:
+        if box is not None and box[0]:
+            for child in box[2]:
+                _release_box(child)
+            _release_box(box)
+    except TypeError:  # interpreter shutdown: the ctypes library object is already gone
+        pass
     obj.handle = None
 
 
