@@ -66,6 +66,7 @@ SIGNATURES = {
     "semlab_ctx_create": (i32, [i32, p, C.POINTER(p)]),
     "semlab_ctx_create_dist": (i32, [i32, p, i32, i32, p, C.POINTER(p)]),
     "semlab_nccl_get_unique_id": (i32, [p]),
+    "semlab_ctx_set_exchange": (i32, [p, i32]),
     "semlab_ctx_destroy": (i32, [p]),
     "semlab_ctx_synchronize": (i32, [p]),
     "semlab_ctx_launch_count": (i64, [p]),

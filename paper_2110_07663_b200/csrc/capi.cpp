@@ -153,10 +153,19 @@ int semlab_ctx_create_dist(int device, void* stream, int rank, int nranks, const
   });
 }
 
+int semlab_ctx_set_exchange(semlab_ctx c, int mode) {
+  return guard([&] {
+    need(c, "semlab_ctx_set_exchange: ctx");
+    if (mode != 0 && mode != 1) invalid("semlab_ctx_set_exchange: mode must be 0 (NCCL) or 1 (peer)");
+    c->exchange_mode = mode;
+  });
+}
+
 int semlab_ctx_destroy(semlab_ctx c) {
   return guard([&] {
     if (!c) return;
     cudaStreamSynchronize(c->stream);
+    c->peer.release();
     if (c->nccl) ncclCommDestroy(static_cast<ncclComm_t>(c->nccl));
     if (c->host_pinned) cudaFreeHost(c->host_pinned);
     if (c->own_stream) cudaStreamDestroy(c->stream);

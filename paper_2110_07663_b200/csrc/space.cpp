@@ -20,6 +20,18 @@ void semlab_ctx_s::allreduce_device(double* d_vals, int K) {
   SB_NCCL(ncclAllReduce(d_vals, d_vals, size_t(K), ncclDouble, ncclSum, static_cast<ncclComm_t>(nccl), stream));
 }
 
+bool semlab_ctx_s::use_peer(int64_t slot_doubles) {
+  if (nranks < 2 || exchange_mode == 0 || peer_state == 0) return false;
+  if (peer_state == 1 && peer.capacity >= slot_doubles) return true;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  SB_CUDA(cudaStreamIsCapturing(stream, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    numeric("peer exchange: mail slots must grow during a CUDA-graph capture (run the operation eagerly first)");
+  // all ranks reach this point for the same exchange (same global plane sizes): collective setup
+  peer_state = peer.init(this, std::max<int64_t>(slot_doubles, peer.capacity)) ? 1 : 0;
+  return peer_state == 1;
+}
+
 void semlab_ctx_s::dots(int K, const double* const* a, const double* const* b, int64_t off, int64_t len,
                         double* host_out, bool global) {
   const double* aa[4];
@@ -32,6 +44,7 @@ void semlab_ctx_s::dots(int K, const double* const* a, const double* const* b, i
   if (global) allreduce_device(dot_out.p, K);
   SB_CUDA(cudaMemcpyAsync(host_pinned, dot_out.p, sizeof(double) * K, cudaMemcpyDeviceToHost, stream));
   sync();
+  if (peer_state == 1) peer.check(this);
   for (int k = 0; k < K; ++k) host_out[k] = host_pinned[k];
 }
 
@@ -121,9 +134,34 @@ void semlab_space_s::build() {
 // rank's partial Q^T sums after a gather-type operation; both ranks add lower + upper partial in
 // that order, so the duplicated planes stay bitwise identical on the two ranks.
 
+// The same exchanges over NVLink peer memory (peer.cu): planes are stored into the neighbour's
+// mail slot and combined there in the same order as below (lower rank's partial first).
+namespace {
+PeerSide side(bool active) {
+  PeerSide p;
+  p.active = active;
+  return p;
+}
+}  // namespace
+
 void semlab_space_s::interface_sum(double* v) {
   if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
+  if (ctx->use_peer(4 * P)) {
+    double* vb = v + sl.lidx(0, 0, int64_t(sl.ez0) * sl.q);
+    double* vt = v + sl.lidx(0, 0, int64_t(sl.ez1) * sl.q);
+    PeerSide sd[2] = {side(sl.nranks_below), side(sl.nranks_above)};
+    sd[0].nsend = sd[0].nrecv = 1;
+    sd[0].src[0] = vb;
+    sd[0].dst[0] = vb;
+    sd[0].op[0] = 1;  // lower partial + mine
+    sd[1].nsend = sd[1].nrecv = 1;
+    sd[1].src[0] = vt;
+    sd[1].dst[0] = vt;
+    sd[1].op[0] = 2;  // mine + upper partial
+    ctx->count(ctx->peer.exchange(ctx, sd, P, ctx->stream));
+    return;
+  }
   if (plane_lo.n < size_t(P)) {
     plane_lo.alloc(size_t(P));
     plane_hi.alloc(size_t(P));
@@ -153,6 +191,27 @@ void semlab_space_s::interface_sum(double* v) {
 void semlab_space_s::interface_sum_halo(double* v) {
   if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
+  if (ctx->use_peer(4 * P)) {
+    const int64_t zb = int64_t(sl.ez0) * sl.q, zt = int64_t(sl.ez1) * sl.q;
+    auto pl = [&](int64_t z) { return v + sl.lidx(0, 0, z); };
+    PeerSide sd[2] = {side(sl.nranks_below), side(sl.nranks_above)};
+    sd[0].nsend = sd[0].nrecv = 2;
+    sd[0].src[0] = pl(zb);
+    sd[0].src[1] = pl(zb + 1);
+    sd[0].dst[0] = pl(zb);
+    sd[0].op[0] = 1;
+    sd[0].dst[1] = pl(zb - 1);  // the ghost plane
+    sd[0].op[1] = 0;
+    sd[1].nsend = sd[1].nrecv = 2;
+    sd[1].src[0] = pl(zt);
+    sd[1].src[1] = pl(zt - 1);
+    sd[1].dst[0] = pl(zt);
+    sd[1].op[0] = 2;
+    sd[1].dst[1] = pl(zt + 1);
+    sd[1].op[1] = 0;
+    ctx->count(ctx->peer.exchange(ctx, sd, P, ctx->stream));
+    return;
+  }
   if (plane_lo.n < size_t(P)) {
     plane_lo.alloc(size_t(P));
     plane_hi.alloc(size_t(P));
@@ -185,6 +244,18 @@ void semlab_space_s::interface_sum_halo(double* v) {
 void semlab_space_s::owner_copy_up_n(double* const* vs, int k) {
   if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
+  if (ctx->use_peer(4 * P)) {
+    PeerSide sd[2] = {side(sl.nranks_below), side(sl.nranks_above)};
+    sd[0].nrecv = k;
+    sd[1].nsend = k;
+    for (int i = 0; i < k; ++i) {
+      sd[0].dst[i] = vs[i] + sl.lidx(0, 0, int64_t(sl.ez0) * sl.q);
+      sd[0].op[i] = 0;
+      sd[1].src[i] = vs[i] + sl.lidx(0, 0, int64_t(sl.ez1) * sl.q);
+    }
+    ctx->count(ctx->peer.exchange(ctx, sd, P, ctx->stream));
+    return;
+  }
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
   cudaStream_t s = ctx->stream;
   const int r = ctx->rank;
@@ -203,6 +274,18 @@ void semlab_space_s::owner_copy_up_n(double* const* vs, int k) {
 void semlab_space_s::halo_exchange(double* v) {
   if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
+  if (ctx->use_peer(4 * P)) {
+    const int64_t zb = int64_t(sl.ez0) * sl.q, zt = int64_t(sl.ez1) * sl.q;
+    PeerSide sd[2] = {side(sl.nranks_below), side(sl.nranks_above)};
+    sd[0].nsend = sd[0].nrecv = 1;
+    sd[0].src[0] = v + sl.lidx(0, 0, zb + 1);
+    sd[0].dst[0] = v + sl.lidx(0, 0, zb - 1);
+    sd[1].nsend = sd[1].nrecv = 1;
+    sd[1].src[0] = v + sl.lidx(0, 0, zt - 1);
+    sd[1].dst[0] = v + sl.lidx(0, 0, zt + 1);
+    ctx->count(ctx->peer.exchange(ctx, sd, P, ctx->stream));
+    return;
+  }
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
   cudaStream_t s = ctx->stream;
   const int r = ctx->rank;
@@ -224,6 +307,11 @@ void semlab_space_s::halo_exchange(double* v) {
 void semlab_space_s::owner_copy_up(double* v) {
   if (!distributed()) return;
   const int64_t P = sl.Nx * sl.Ny;
+  if (ctx->use_peer(4 * P)) {
+    double* vs[1] = {v};
+    owner_copy_up_n(vs, 1);
+    return;
+  }
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
   cudaStream_t s = ctx->stream;
   const int r = ctx->rank;

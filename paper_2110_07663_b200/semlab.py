@@ -101,6 +101,10 @@ class Context:
     def synchronize(self):
         check(lib.semlab_ctx_synchronize(self.handle))
 
+    def set_exchange(self, peer: bool) -> None:
+        """z-slab exchanges over NVLink peer memory (True, default when available) or NCCL."""
+        check(lib.semlab_ctx_set_exchange(self.handle, 1 if peer else 0))
+
     @property
     def launch_count(self) -> int:
         return int(lib.semlab_ctx_launch_count(self.handle))

@@ -47,6 +47,8 @@ def main():
         return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
 
     out = {"world": world}
+    if os.environ.get("DIST_EXCHANGE", "peer") == "nccl":
+        ctx.set_exchange(False)
     mesh = S.generate_kershaw(eps, E, ctx)
     sp = S.SemSpace(mesh, p)
     c = o.SemSpace(o.generate_kershaw(eps, E), p)
@@ -132,6 +134,16 @@ def main():
     out["gmres_iters"] = [st.iterations, sto.iterations]
     out["gmres_conv"] = bool(st.converged)
     out["gmres_x"] = rel(gather(x), xo)
+    # the NVLink peer-memory exchanges and NCCL send/recv give bitwise the same results
+    if os.environ.get("DIST_EXCHANGE", "peer") == "peer":
+        w_peer = sp.apply_A(u[sl.local_slice()])
+        z_peer = pm.vcycle(b_loc).clone()
+        ctx.set_exchange(False)
+        w_nccl = sp.apply_A(u[sl.local_slice()])
+        pm_n = S.Pmg(mesh, (7, 3, 1), S.RAS_SMOOTHER, 2, 0.1, 1.1, 64, S.COARSE_DIRECT)
+        z_nccl = pm_n.vcycle(b_loc)
+        ctx.set_exchange(True)
+        out["peer_vs_nccl_bitwise"] = bool(torch.equal(w_peer, w_nccl) and torch.equal(z_peer, z_nccl))
     # the bench setting on slabs: FP32 smoother (fused slab Chebyshev-RAS, FP32-factor Ax), FP64 GMRES
     pm32 = S.Pmg(mesh, (7, 3, 1), S.RAS_SMOOTHER, 2, 0.1, 1.1, 32, S.COARSE_AMG)
     pmo_amg = o.Pmg(o.generate_kershaw(eps, E), (7, 3, 1), "ras", 2, 0.1, 1.1, "amg", 64)

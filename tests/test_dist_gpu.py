@@ -16,12 +16,14 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("nproc,E", [(2, 4), (4, 4), (2, 8), (4, 8)])
-def test_distributed_matches_oracle(nproc, E):
-    """E=4: one or two element layers per rank; E=8: two or four."""
+@pytest.mark.parametrize("nproc,E,exchange", [(2, 4, "peer"), (4, 4, "peer"), (2, 8, "peer"), (4, 8, "peer"),
+                                               (2, 4, "nccl"), (4, 8, "nccl")])
+def test_distributed_matches_oracle(nproc, E, exchange):
+    """E=4: one or two element layers per rank; E=8: two or four. exchange: the z-slab plane
+    exchanges over NVLink peer memory (default) or NCCL send/recv."""
     if _ngpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    env = dict(os.environ, DIST_E=str(E), DIST_EPS="0.3")
+    env = dict(os.environ, DIST_E=str(E), DIST_EPS="0.3", DIST_EXCHANGE=exchange)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "dist_worker.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
@@ -49,3 +51,5 @@ def test_distributed_matches_oracle(nproc, E):
     it, ito = r["gmres_iters"]
     assert r["gmres_conv"] and abs(it - ito) <= 1
     assert r["gmres_x"] < 1e-10
+    if exchange == "peer":
+        assert r["peer_vs_nccl_bitwise"], r
