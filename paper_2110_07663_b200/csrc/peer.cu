@@ -140,12 +140,12 @@ struct PeerLinks::Impl {
 
 PeerLinks::~PeerLinks() { release(); }
 
+// The rank's own mail is never freed while the process lives: a neighbour that is still finishing
+// its last receive may store an acknowledgement into it after this rank has moved on (a few MB).
 void PeerLinks::release() {
   if (!impl) return;
   for (auto& p : impl->peer_mail)
     if (p) cudaIpcCloseMemHandle(p);
-  if (impl->mail) cudaFree(impl->mail);
-  if (impl->ctl) cudaFree(impl->ctl);
   delete impl;
   impl = nullptr;
 }
@@ -167,6 +167,12 @@ bool PeerLinks::supported(semlab_ctx c) {
 // (NCCL all-gather of the 64-byte handles) and map the z-neighbours' mail. The peer path is used
 // only if every rank can (NCCL min-reduction of the local verdicts); otherwise false (NCCL path).
 bool PeerLinks::init(semlab_ctx c, int64_t slot_doubles) {
+  if (impl) {  // growth: every rank's earlier exchanges have drained (barrier) before the switch
+    DevBuf<double> one(1);
+    one.zero(c->stream);
+    SB_NCCL(ncclAllReduce(one.p, one.p, 1, ncclDouble, ncclSum, static_cast<ncclComm_t>(c->nccl), c->stream));
+    SB_CUDA(cudaStreamSynchronize(c->stream));
+  }
   release();
   {
     DevBuf<double> ok(1);
