@@ -179,6 +179,7 @@ int semlab_ctx_synchronize(semlab_ctx c) {
   return guard([&] {
     need(c, "semlab_ctx_synchronize: ctx");
     c->sync();
+    if (c->peer_state == 1) c->peer.check(c);
   });
 }
 
