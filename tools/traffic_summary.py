@@ -37,8 +37,8 @@ def main():
             "parts": {"k_axe<double>": a64, "k_axe<float>": a32, "k_face_epi7": face_b["EWrite"], "k_rasw": r0},
             "sources": [os.path.basename(x) for x in sys.argv[1:5]],
             "note": "ncu --set full (caches flushed between kernels: cold-cache traffic), one launch each"}
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
-                        "latest_ncu_summary.json")
+    path = sys.argv[5] if len(sys.argv) > 5 else os.path.join(
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "latest_ncu_summary.json")
     json.dump(summ, open(path, "w"), indent=1)
     print(json.dumps(summ, indent=1))
 
