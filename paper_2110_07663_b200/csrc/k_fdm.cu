@@ -820,13 +820,10 @@ void prep(K kern, size_t smem) {
   smem_attr(kern, smem);
 }
 
-bool ras_warp() {
-  static const bool on = [] {
-    const char* e = std::getenv("SEMLAB_RAS_WARP");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+#ifndef SEMLAB_RAS_WARP
+#define SEMLAB_RAS_WARP 1  // build-time A/B (tools/build_variant*.sh): 0 = CTA-per-group RAS for every order
+#endif
+constexpr bool ras_warp() { return SEMLAB_RAS_WARP != 0; }
 
 template <class T>
 struct Launch {

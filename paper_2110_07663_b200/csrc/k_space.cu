@@ -175,14 +175,10 @@ __global__ void k_geom(const Slab sl, const DMat<ND> Dm, const W1<ND> w1, const 
 }
 
 // ------------------------------------------------------------------------ Ax
-// SEMLAB_AX_PERSISTENT=0 selects the one-CTA-per-element kernel (kept for A/B measurement).
-bool ax_persistent() {
-  static const bool on = [] {
-    const char* e = std::getenv("SEMLAB_AX_PERSISTENT");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+#ifndef SEMLAB_AX_PERSISTENT
+#define SEMLAB_AX_PERSISTENT 1  // build-time A/B: 0 = one CTA per element group (orders != 7)
+#endif
+constexpr bool ax_persistent() { return SEMLAB_AX_PERSISTENT != 0; }
 
 template <int ND>
 constexpr int ax_min_blocks() {  // occupancy target: caps registers so ~20 warps/SM stay resident
@@ -1060,13 +1056,10 @@ int64_t axw_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
   return 2;
 }
 
-bool ax_dmma() {  // SEMLAB_AX_DMMA=0 selects the FP64-FMA persistent kernel (A/B measurement)
-  static const bool on = [] {
-    const char* e = std::getenv("SEMLAB_AX_DMMA");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+#ifndef SEMLAB_AX_DMMA
+#define SEMLAB_AX_DMMA 1  // build-time A/B: 0 = the FP64-FMA persistent kernel at p = 7
+#endif
+constexpr bool ax_dmma() { return SEMLAB_AX_DMMA != 0; }
 
 // Q^T of element-local results with an owner epilogue: each lattice node sums its <= 8
 // contributors in ascending element id (sem_space.cpp:110-119 order), masked nodes get 0.

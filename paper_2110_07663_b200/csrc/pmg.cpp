@@ -553,14 +553,10 @@ semlab_pmg_s::~semlab_pmg_s() {
   delete coarse_full;
 }
 
-// SEMLAB_SMOOTHER_GEOM32=0 keeps FP64 geometric factors in the FP32 smoother (A/B measurement).
-static bool smoother_geom32() {
-  static const bool on = [] {
-    const char* e = std::getenv("SEMLAB_SMOOTHER_GEOM32");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+#ifndef SEMLAB_SMOOTHER_GEOM32
+#define SEMLAB_SMOOTHER_GEOM32 1  // build-time A/B: 0 = FP64 factors in the FP32 smoother's operator
+#endif
+static constexpr bool smoother_geom32() { return SEMLAB_SMOOTHER_GEOM32 != 0; }
 
 void semlab_pmg_s::build() {
   const size_t nl = orders.size();
@@ -756,14 +752,10 @@ void semlab_pmg_s::cycle_additive(int l) {
   prolong(l, lv[size_t(l) + 1].x.p, L.x.p, true);
 }
 
-// SEMLAB_PMG_GRAPH=0 launches the V-cycle kernel by kernel instead of as a CUDA graph.
-static bool pmg_graph_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("SEMLAB_PMG_GRAPH");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+#ifndef SEMLAB_PMG_GRAPH
+#define SEMLAB_PMG_GRAPH 1  // build-time A/B: 0 = the V-cycle launched kernel by kernel
+#endif
+static constexpr bool pmg_graph_enabled() { return SEMLAB_PMG_GRAPH != 0; }
 
 // The V-cycle body works on the hierarchy's own buffers only (the input and output are copied
 // in and out), so after one eager warm-up call (lazy allocations, per-kernel launch setup) it is

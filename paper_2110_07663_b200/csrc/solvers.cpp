@@ -22,14 +22,10 @@ cudaStream_t st(semlab_ctx c) { return c->stream; }
 
 // Fused Chebyshev-Jacobi needs S = diag(A)^-1 of the same space and a single rank (interface
 // planes need the cross-rank sum before the owner epilogue).
-// SEMLAB_DIST_FUSED=0 keeps the generic Chebyshev path on z-slabs (A/B).
-bool dist_ras_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("SEMLAB_DIST_FUSED");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+#ifndef SEMLAB_DIST_FUSED
+#define SEMLAB_DIST_FUSED 1  // build-time A/B: 0 = the generic Chebyshev path on z-slabs
+#endif
+constexpr bool dist_ras_enabled() { return SEMLAB_DIST_FUSED != 0; }
 
 // The fused paths apply A through the Ax epilogues, which do not remove the mean: Neumann
 // spaces (sem_space.cpp:207) take the generic path (A->apply, then S->apply).
