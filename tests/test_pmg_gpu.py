@@ -162,19 +162,15 @@ np.save(sys.argv[1], np.stack(outs))
 
 def test_vcycle_graph_replay_is_bitwise_eager(tmp_path):
     """The captured CUDA-graph V-cycle (pmg.cpp run_cycle) replays exactly the eager cycle: the
-    FP32-smoother V-cycle output is bitwise identical with SEMLAB_PMG_GRAPH=1 and =0, and across
-    replays."""
+    first call runs eagerly, the second captures and launches the graph, later calls replay it;
+    the FP32-smoother V-cycle outputs are bitwise identical."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for g in ("1", "0"):
-        f = tmp_path / f"v{g}.npy"
-        env = dict(os.environ, SEMLAB_PMG_GRAPH=g)
-        subprocess.run([sys.executable, "-c", _GRAPH_SCRIPT % root, str(f)], check=True, env=env, timeout=600)
-        res[g] = np.load(f)
-    for k in range(4):
-        assert np.array_equal(res["1"][k], res["0"][0])
-        assert np.array_equal(res["0"][k], res["0"][0])
+    f = tmp_path / "v.npy"
+    subprocess.run([sys.executable, "-c", _GRAPH_SCRIPT % root, str(f)], check=True, timeout=600)
+    res = np.load(f)
+    for k in range(1, 4):
+        assert np.array_equal(res[k], res[0])
