@@ -746,6 +746,17 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
+// Face-buffer stores keep their lines in L2 (evict_last): the face gather reads them back right
+// after, while the geometry streams past with evict-first loads, so the 78 MB buffer need not
+// round-trip through HBM.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_l2_keep(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 // compact index of a face node (i, j, k) of an 8^3 element (at least one coordinate is 0 or 7)
 __device__ __forceinline__ int face_idx(int i, int j, int k) {
   if (k == 0) return j * 8 + i;
@@ -922,6 +933,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
     }
     // epilogue: interior nodes (one contributor) now, face nodes to the face buffer
     {
+      const uint64_t keep = l2_evict_last_policy();
       const bool jface = (j == 0 || j == q);
       double* fe = fb + size_t(el) * FACE;
 #pragma unroll
@@ -939,7 +951,7 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
           const bool face = jface || k == 0 || k == q || i == 0 || i == q;
           const double v = o[2 * k + t % 2];
           if (face)
-            fe[face_idx(i, j, k)] = v;
+            st_l2_keep(fe + face_idx(i, j, k), v, keep);
           else
             epi.store(g0 + k * NxNy + t % 2, in[t], v);
         }
