@@ -242,6 +242,7 @@ def run_ours(args, cfg, name):
         uid = [S.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx = S.Context(local, stream, rank, world, uid[0])
+        ctx.set_exchange(args.exchange == "peer")
     else:
         ctx = S.Context(local, stream)
 
@@ -489,7 +490,7 @@ def run_ours(args, cfg, name):
                 "config": {"workload": describe(name, cfg), "n_dofs": n_global, "elements": cfg["E"] ** 3,
                            "order": cfg["p"], "iterations_per_solve": iters / args.steps, "converged": conv,
                            "max_rel_residual": rel, "smoother_precision": f"fp{cfg['precision']}",
-                           "krylov_precision": "fp64", "parallelism": f"z-slab x{world}", "setup_s": setup_s,
+                           "krylov_precision": "fp64", "parallelism": f"z-slab x{world}" + (f", {args.exchange} exchanges" if world > 1 else ""), "setup_s": setup_s,
                            "l2": "inputs larger than L2 (geometry 805 MB at E=32^3)",
                            "time_to_1e-8_ms": t / args.steps * 1e3, "step_wall_ms": [round(v, 1) for v in step_ms]},
                 "e2e": e2e, "roofline": dominant, "rooflines": roofs, "rooflines_skipped": skipped or None,
@@ -512,6 +513,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=0,
                     help="iterations of the reference timed for cpu_baseline after its setup (0: sized to the mesh)")
     ap.add_argument("--no-fp64-line", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="z-slab plane exchanges: NCCL send/recv or NVLink peer-memory mail slots")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("timing rules: --warmup must be >= 3")

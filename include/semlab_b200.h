@@ -114,9 +114,9 @@ int semlab_ctx_create(int device, void* cuda_stream, semlab_ctx* out);
 int semlab_ctx_create_dist(int device, void* cuda_stream, int rank, int nranks,
                            const void* nccl_id, semlab_ctx* out);
 int semlab_nccl_get_unique_id(void* out128);
-/* z-slab neighbour exchanges (interface sums, Schwarz halos, owner copy-ups): 1 (default) over
-   NVLink peer memory (CUDA IPC mail slots + flags) when every rank can map its neighbours, else
-   NCCL; 0 NCCL send/recv only. Set on every rank before the first exchange. */
+/* z-slab neighbour exchanges (interface sums, Schwarz halos, owner copy-ups): 0 (default) NCCL
+   send/recv; 1 NVLink peer memory (CUDA IPC mail slots + flag/ack protocol) when every rank can
+   map its neighbours, else NCCL. Set on every rank, in the same order, before the exchanges. */
 int semlab_ctx_set_exchange(semlab_ctx ctx, int mode);
 int semlab_ctx_destroy(semlab_ctx ctx);
 int semlab_ctx_synchronize(semlab_ctx ctx);

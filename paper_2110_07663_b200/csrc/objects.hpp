@@ -27,10 +27,10 @@ struct semlab_ctx_s {
   // per solve costs a device sync and tens to hundreds of ms. A nested solve allocates its own.
   sb::DevBuf<double> krylov_ws;
   bool krylov_ws_busy = false;
-  // z-slab neighbour exchanges: over NVLink peer memory (sb::PeerLinks) when every rank supports
-  // it, else NCCL send/recv. exchange_mode: 1 peer when possible (default), 0 NCCL only.
+  // z-slab neighbour exchanges: NCCL send/recv (exchange_mode 0, the default: measured faster), or
+  // NVLink peer memory (sb::PeerLinks, exchange_mode 1) when every rank supports it.
   sb::PeerLinks peer;
-  int exchange_mode = 1, peer_state = -1;  // -1 undecided, 0 NCCL, 1 peer
+  int exchange_mode = 0, peer_state = -1;  // peer_state: -1 undecided, 0 NCCL, 1 peer
   bool use_peer(int64_t slot_doubles);     // collective on first use / growth (never inside a capture)
   sb::DotScratch dots() const { return {dot_partial.p, dot_counter.p}; }
   void count(int64_t n) { launches += n; }

@@ -35,15 +35,21 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 
 // spin until *p >= v (acquire); false on timeout
 __device__ bool wait_geq(const unsigned long long* p, unsigned long long v, unsigned* err) {
+  if (ld_acquire_sys(p) >= v) return true;
   const long long t0 = clock64();
-  while (ld_acquire_sys(p) < v) {
-    __nanosleep(200);
+  for (unsigned it = 0;; ++it) {
+    if (ld_acquire_sys(p) >= v) return true;
+    if (it > 4096) __nanosleep(64);
     if (clock64() - t0 > (long long)20000000000LL) {  // ~10 s at 2 GHz
       atomicExch(err, 1u);
       return false;
     }
   }
-  return true;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
 struct Side {                   // one direction of one exchange
@@ -77,11 +83,13 @@ __global__ void k_peer_send(Side s0, Side s1, int64_t P, int64_t slot_doubles, i
   for (int k = 0; k < s.n; ++k)
     for (int64_t t = int64_t(b) * blockDim.x + threadIdx.x; t < P; t += int64_t(G) * blockDim.x)
       slot[k * P + t] = s.src[k][t];
-  __threadfence_system();
+  // the block's stores -> (barrier) -> thread 0's acq_rel counter -> the last block's system-scope
+  // release of the flag: cumulative, so the neighbour's acquire of the flag sees every store
   __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(s.done, 1u) == unsigned(G) - 1) {
+  if (threadIdx.x == 0 && atom_add_acq_rel_gpu(s.done, 1u) == unsigned(G) - 1) {
     *s.done = 0;
     *s.seq = seq;
+    __threadfence_system();
     st_release_sys(s.flags + (seq - 1) % K, seq);
   }
 }
@@ -109,10 +117,9 @@ __global__ void k_peer_recv(Side s0, Side s1, int64_t P, int64_t slot_doubles, i
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(s.done, 1u) == unsigned(G) - 1) {
+  if (threadIdx.x == 0 && atom_add_acq_rel_gpu(s.done, 1u) == unsigned(G) - 1) {
     *s.done = 0;
     *s.seq = seq;
-    __threadfence_system();
     st_release_sys(s.ack, seq);  // the sender may reuse the slot
   }
 }
@@ -262,7 +269,7 @@ int64_t PeerLinks::exchange(semlab_ctx c, const PeerSide* sides, int64_t P, cuda
     b.seq = impl->ctl + 2 + d;
     b.done = reinterpret_cast<unsigned*>(impl->ctl + 4) + 2 + d;
   }
-  const int G = int(std::min<int64_t>(32, std::max<int64_t>(1, (P + 4095) / 4096)));
+  const int G = int(std::min<int64_t>(64, std::max<int64_t>(1, (P + 1023) / 1024)));
   k_peer_send<<<2 * G, 256, 0, s>>>(snd[0], snd[1], P, SD, K, impl->err);
   SB_LAUNCH_CHECK();
   k_peer_recv<<<2 * G, 256, 0, s>>>(rcv[0], rcv[1], P, SD, K, impl->err);

@@ -102,7 +102,7 @@ class Context:
         check(lib.semlab_ctx_synchronize(self.handle))
 
     def set_exchange(self, peer: bool) -> None:
-        """z-slab exchanges over NVLink peer memory (True, default when available) or NCCL."""
+        """z-slab exchanges over NVLink peer memory (True, when every rank can) or NCCL (default)."""
         check(lib.semlab_ctx_set_exchange(self.handle, 1 if peer else 0))
 
     @property

@@ -47,8 +47,7 @@ def main():
         return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
 
     out = {"world": world}
-    if os.environ.get("DIST_EXCHANGE", "peer") == "nccl":
-        ctx.set_exchange(False)
+    ctx.set_exchange(os.environ.get("DIST_EXCHANGE", "peer") == "peer")
     mesh = S.generate_kershaw(eps, E, ctx)
     sp = S.SemSpace(mesh, p)
     c = o.SemSpace(o.generate_kershaw(eps, E), p)
