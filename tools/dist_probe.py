@@ -20,6 +20,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = S.Context(rank, stream, rank, world, uid[0])
+    ctx.set_exchange(os.environ.get("EXCHANGE", "nccl") == "peer")
     E = int(os.environ.get("E", "32"))
     mesh = S.generate_kershaw(0.3, E, ctx)
     pmg = S.Pmg(mesh, (7, 3, 1), S.RAS_SMOOTHER, 2, 0.1, 1.1, 32, S.COARSE_AMG)
@@ -53,7 +54,7 @@ def main():
     res["gmres"] = timeit(solve, 2)
     res["iters"] = st.iterations
     if rank == 0:
-        print(f"world={world} E={E}: " + ", ".join(f"{k}={v:.3f}" + ("" if k == "iters" else "ms") for k, v in res.items()),
+        print(f"world={world} E={E} exchange={os.environ.get('EXCHANGE', 'nccl')}: " + ", ".join(f"{k}={v:.3f}" + ("" if k == "iters" else "ms") for k, v in res.items()),
               flush=True)
     dist.barrier()
 
