@@ -37,6 +37,11 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
                                               const int mask_out, const Grid3 gmask_out, const int zb, const int nz,
                                               const int add_out, const double* __restrict__ sub_from) {
   const int qf = QF > 0 ? QF : qf_rt, qc = QC > 0 ? QC : qc_rt;
+  // J from shared memory: the threads of a warp index different rows (i), which the kernel-
+  // parameter (constant) bank would serialise
+  __shared__ double sJ[16 * 16];
+  for (int t = threadIdx.x; t < (qf + 1) * (qc + 1); t += blockDim.x) sJ[t] = J.v[t];
+  __syncthreads();
   const unsigned nx = unsigned(gout.N[0]), ny = unsigned(gout.N[1]);
   const unsigned total = nx * ny * unsigned(nz);
   const int jn = qc + 1;  // J is (qf+1) x (qc+1), row-major
@@ -79,7 +84,7 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
 #pragma unroll
       for (int a = 0; a < (QC > 0 ? QC + 1 : 16); ++a) {
         if (QC == 0 && a >= jn) break;
-        const double w = J.v[i * jn + a];
+        const double w = sJ[i * jn + a];
         if (w != 0.0) acc += w * fetch(e * qc + a);
       }
     } else {
@@ -93,14 +98,14 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
 #pragma unroll
           for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
             if (QF == 0 && i > qf) break;
-            const double w = J.v[i * jn + qc];
+            const double w = sJ[i * jn + qc];
             if (w != 0.0) acc += w * fetch((e - 1) * qf + i);
           }
         if (e < E_axis && e < J.e_hi)
 #pragma unroll
           for (int i = 1; i < (QF > 0 ? QF + 1 : 16); ++i) {
             if (QF == 0 && i > qf) break;
-            const double w = J.v[i * jn + 0];
+            const double w = sJ[i * jn + 0];
             if (w != 0.0) acc += w * fetch(e * qf + i);
           }
       } else {
@@ -109,7 +114,7 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
 #pragma unroll
         for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
           if (QF == 0 && i > qf) break;
-          const double w = J.v[i * jn + aa];
+          const double w = sJ[i * jn + aa];
           if (w != 0.0) acc += w * fetch(e * qf + i);
         }
       }
