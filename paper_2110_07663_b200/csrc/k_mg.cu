@@ -37,11 +37,6 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
                                               const int mask_out, const Grid3 gmask_out, const int zb, const int nz,
                                               const int add_out, const double* __restrict__ sub_from) {
   const int qf = QF > 0 ? QF : qf_rt, qc = QC > 0 ? QC : qc_rt;
-  // J from shared memory: the threads of a warp index different rows (i), which the kernel-
-  // parameter (constant) bank would serialise
-  __shared__ double sJ[16 * 16];
-  for (int t = threadIdx.x; t < (qf + 1) * (qc + 1); t += blockDim.x) sJ[t] = J.v[t];
-  __syncthreads();
   const unsigned nx = unsigned(gout.N[0]), ny = unsigned(gout.N[1]);
   const unsigned total = nx * ny * unsigned(nz);
   const int jn = qc + 1;  // J is (qf+1) x (qc+1), row-major
@@ -67,11 +62,18 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
         if (d != AXIS) other_bnd = other_bnd || c[d] == 0 || c[d] == gmask_in.N[d] - 1;
     }
     const bool min_ = mask_in && gmask_in.dirichlet;
+    // branch-free: both loads always issue (coord is inside the lattice) and the mask selects, so
+    // the compiler can put the whole 1-D support's loads in flight together
+    const double* row_s = row_sub ? row_sub : row_in;
+    const bool has_sub = row_sub != nullptr;
     auto fetch = [&](int coord) -> double {
-      if (min_ && (other_bnd || coord == 0 || coord == nax_in - 1)) return 0.0;
+      const double a = __ldg(row_in + coord * sin), b = __ldg(row_s + coord * sin);
       // sub_from: the input is (sub_from - in), e.g. the residual b - A x fused into Pᵀ
-      return row_sub ? row_sub[coord * sin] - row_in[coord * sin] : row_in[coord * sin];
+      const double v = has_sub ? b - a : a;
+      return (min_ && (other_bnd || coord == 0 || coord == nax_in - 1)) ? 0.0 : v;
     };
+    // every weight is applied, zero or not (w = 0 adds exactly +0): a branch on w would keep the
+    // compiler from issuing the support loads together, and the pass would be load-latency bound
     const int X = c[AXIS];
     double acc = 0.0;
     if (PROLONG) {
@@ -84,8 +86,8 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
 #pragma unroll
       for (int a = 0; a < (QC > 0 ? QC + 1 : 16); ++a) {
         if (QC == 0 && a >= jn) break;
-        const double w = sJ[i * jn + a];
-        if (w != 0.0) acc += w * fetch(e * qc + a);
+        const double w = J.v[i * jn + a];
+        acc += w * fetch(e * qc + a);
       }
     } else {
       const int I = X;
@@ -98,15 +100,15 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
 #pragma unroll
           for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
             if (QF == 0 && i > qf) break;
-            const double w = sJ[i * jn + qc];
-            if (w != 0.0) acc += w * fetch((e - 1) * qf + i);
+            const double w = J.v[i * jn + qc];
+            acc += w * fetch((e - 1) * qf + i);
           }
         if (e < E_axis && e < J.e_hi)
 #pragma unroll
           for (int i = 1; i < (QF > 0 ? QF + 1 : 16); ++i) {
             if (QF == 0 && i > qf) break;
-            const double w = sJ[i * jn + 0];
-            if (w != 0.0) acc += w * fetch(e * qf + i);
+            const double w = J.v[i * jn + 0];
+            acc += w * fetch(e * qf + i);
           }
       } else {
         if (e == E_axis) e -= 1;  // last coarse node belongs to the last element
@@ -114,8 +116,8 @@ __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, con
 #pragma unroll
         for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
           if (QF == 0 && i > qf) break;
-          const double w = sJ[i * jn + aa];
-          if (w != 0.0) acc += w * fetch(e * qf + i);
+          const double w = J.v[i * jn + aa];
+          acc += w * fetch(e * qf + i);
         }
       }
     }

@@ -989,10 +989,13 @@ __device__ __forceinline__ Cand2 cand2(int c, int q, int lo_e, int hi_e) {
   return r;
 }
 
-// One face lattice node (x, y, z): sum its contributors' face-buffer entries in ascending element
-// id — the (lower, upper) candidates of z, then y, then x, all eight loads predicated and issued
-// together — apply the Dirichlet mask and the epilogue.
-template <class EpiT>
+// One face lattice node (x, y, z) of family FAM: sum its contributors' face-buffer entries in
+// ascending element id — the (lower, upper) candidates of z, then y, then x, the loads predicated
+// and issued together — apply the Dirichlet mask and the epilogue. The family fixes which axes
+// can split (FAM 0: z on an element face, x and y any; FAM 1: z interior, y on a face, x any;
+// FAM 2: z and y interior, x on a face), so only the 8 / 4 / 2 possible contributors are formed
+// and their face indices reduce to the closed forms of face_idx for that face.
+template <int FAM, class EpiT>
 __device__ __forceinline__ void face_node7(const Slab& sl, const double* __restrict__ fb, const EpiT& epi, int x,
                                            int y, int z) {
   using namespace axw;
@@ -1002,23 +1005,56 @@ __device__ __forceinline__ void face_node7(const Slab& sl, const double* __restr
     epi(g, 0.0);
     return;
   }
-  const Cand2 cx = cand2(x, q, 0, sl.Ex), cy = cand2(y, q, 0, sl.Ey), cz = cand2(z, q, sl.ez0, sl.ez1);
-  double v[8];
+  constexpr int NC = FAM == 0 ? 8 : (FAM == 1 ? 4 : 2);
+  double v[NC];
+  if constexpr (FAM == 0) {
+    const Cand2 cx = cand2(x, q, 0, sl.Ex), cy = cand2(y, q, 0, sl.Ey);
+    const int ezu = z / q - sl.ez0;  // upper element layer (local k = 0); lower: ezu - 1 (k = q)
+    const bool zv[2] = {ezu - 1 >= 0, ezu < sl.ez1 - sl.ez0};
 #pragma unroll
-  for (int c = 0; c < 2; ++c)
+    for (int c = 0; c < 2; ++c)
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+      for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const bool on = (c ? cz.v1 : cz.v0) && (b ? cy.v1 : cy.v0) && (a ? cx.v1 : cx.v0);
-        const int ez = (c ? cz.e1 : cz.e0) - sl.ez0, ey = b ? cy.e1 : cy.e0, ex = a ? cx.e1 : cx.e0;
-        const int el = ex + sl.Ex * (ey + sl.Ey * ez);
-        const double* p = fb + size_t(el) * FACE + face_idx(a ? cx.l1 : cx.l0, b ? cy.l1 : cy.l0, c ? cz.l1 : cz.l0);
-        v[c * 4 + b * 2 + a] = on ? __ldcs(p) : 0.0;
+        for (int aa = 0; aa < 2; ++aa) {
+          const bool on = zv[c] && (bb ? cy.v1 : cy.v0) && (aa ? cx.v1 : cx.v0);
+          const int ey = bb ? cy.e1 : cy.e0, ex = aa ? cx.e1 : cx.e0;
+          const int el = ex + sl.Ex * (ey + sl.Ey * (ezu - 1 + c));
+          const int fi = (c ? 0 : 64) + (bb ? cy.l1 : cy.l0) * 8 + (aa ? cx.l1 : cx.l0);
+          v[c * 4 + bb * 2 + aa] = on ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
+        }
+  } else {
+    const int ez = z / q, k = z - ez * q;  // interior layer k = 1 .. q-1 of element layer ez
+    const int zb = 128 + (k - 1) * 28;
+    if constexpr (FAM == 1) {
+      const Cand2 cx = cand2(x, q, 0, sl.Ex);
+      const int eyu = y / q;  // upper element row (j = 0); lower: eyu - 1 (j = q)
+      const bool yv[2] = {eyu - 1 >= 0, eyu < sl.Ey};
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int aa = 0; aa < 2; ++aa) {
+          const bool on = yv[bb] && (aa ? cx.v1 : cx.v0);
+          const int ex = aa ? cx.e1 : cx.e0;
+          const int el = ex + sl.Ex * (eyu - 1 + bb + sl.Ey * (ez - sl.ez0));
+          const int fi = zb + (bb ? 0 : 8) + (aa ? cx.l1 : cx.l0);
+          v[bb * 2 + aa] = on ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
+        }
+    } else {
+      const int ey = y / q, j = y - ey * q;  // interior row j = 1 .. q-1
+      const int exu = x / q;                  // upper element (i = 0); lower: exu - 1 (i = q)
+      const bool xv[2] = {exu - 1 >= 0, exu < sl.Ex};
+#pragma unroll
+      for (int aa = 0; aa < 2; ++aa) {
+        const int el = exu - 1 + aa + sl.Ex * (ey + sl.Ey * (ez - sl.ez0));
+        const int fi = zb + 16 + 2 * (j - 1) + (aa ? 0 : 1);
+        v[aa] = xv[aa] ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
       }
+    }
+  }
   double acc = 0.0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) acc += v[k];  // ascending element id; absent contributors add +0.0
+  for (int c = 0; c < NC; ++c) acc += v[c];  // ascending element id; absent contributors add +0.0
   epi(g, acc);
 }
 
@@ -1027,21 +1063,31 @@ __device__ __forceinline__ void face_node7(const Slab& sl, const double* __restr
 //   z % q == 0 (FAM 0): rows y = 0 .. Ny-1, threads over x
 //   z % q != 0: rows 0 .. Ey  are FAM 1 (y = q row, threads over x);
 //               rows Ey+1 .. 2Ey are FAM 2 (y in element row ey = row-Ey-1, threads over (i, y-1-q ey))
+#ifndef SEMLAB_FACE_BLOCKS
+#define SEMLAB_FACE_BLOCKS (148 * 64)  // face-pass blocks (each walks rows with stride gridDim.y)
+#endif
 template <class EpiT>
 __global__ void __launch_bounds__(128) k_face_epi7(const Slab sl, const double* __restrict__ fb, const EpiT epi) {
   constexpr int q = 7;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int zz = int(blockIdx.z), z = sl.ez0 * q + zz, row = int(blockIdx.y);
-  if (zz % q == 0) {
-    if (t >= sl.Nx || row >= sl.Ny) return;
-    face_node7(sl, fb, epi, t, row, z);
-  } else if (row <= sl.Ey) {
-    if (t >= sl.Nx) return;
-    face_node7(sl, fb, epi, t, row * q, z);
-  } else {
-    const int i = t / (q - 1), yi = t - i * (q - 1);
-    if (i > sl.Ex || row > 2 * sl.Ey) return;
-    face_node7(sl, fb, epi, i * q, (row - sl.Ey - 1) * q + 1 + yi, z);
+  // compact row list: the Ny rows of each of the nzl+1 planes z % q == 0, then the 2 Ey + 1 face
+  // rows of each of the 6 nzl planes between them; a block walks rows with stride gridDim.y
+  const int ra = (sl.ez1 - sl.ez0 + 1) * sl.Ny, rb = 2 * sl.Ey + 1;
+  const int rows = ra + (sl.ez1 - sl.ez0) * (q - 1) * rb;
+  for (int r = int(blockIdx.y); r < rows; r += int(gridDim.y)) {
+    if (r < ra) {
+      const int pz = r / sl.Ny, row = r - pz * sl.Ny;
+      if (t < sl.Nx) face_node7<0>(sl, fb, epi, t, row, (sl.ez0 + pz) * q);
+      continue;
+    }
+    const int rr = r - ra, pl = rr / rb, row = rr - pl * rb;
+    const int ez = pl / (q - 1), z = (sl.ez0 + ez) * q + 1 + (pl - ez * (q - 1));
+    if (row <= sl.Ey) {
+      if (t < sl.Nx) face_node7<1>(sl, fb, epi, t, row * q, z);
+    } else {
+      const int i = t / (q - 1), yi = t - i * (q - 1);
+      if (i <= sl.Ex) face_node7<2>(sl, fb, epi, i * q, (row - sl.Ey - 1) * q + 1 + yi, z);
+    }
   }
 }
 
@@ -1062,8 +1108,9 @@ int64_t axw_launch(const Slab& sl, const double* u, const GT* geom, const AxSync
   SB_LAUNCH_CHECK();
   const unsigned nzl = unsigned(sl.ez1 - sl.ez0);
   const unsigned bx = unsigned((std::max<int64_t>(sl.Nx, (sl.Ex + 1) * 6) + 127) / 128);
-  const unsigned by = unsigned(std::max<int64_t>(sl.Ny, 2 * sl.Ey + 1));
-  k_face_epi7<<<dim3(bx, by, nzl * 7 + 1), 128, 0, s>>>(sl, sy.dep, epi);
+  const int64_t rows = int64_t(nzl + 1) * sl.Ny + int64_t(nzl) * 6 * (2 * sl.Ey + 1);
+  const unsigned by = unsigned(std::min<int64_t>(rows, std::max<int64_t>(1, SEMLAB_FACE_BLOCKS / bx)));
+  k_face_epi7<<<dim3(bx, by), 128, 0, s>>>(sl, sy.dep, epi);
   SB_LAUNCH_CHECK();
   return 2;
 }
