@@ -19,110 +19,310 @@ namespace {
 
 int grid_for(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148LL * 32))); }
 
-__device__ __forceinline__ bool on_boundary(int64_t x, int64_t y, int64_t z, const Grid3& g) {
-  return x == 0 || x == g.N[0] - 1 || y == 0 || y == g.N[1] - 1 || z == 0 || z == g.N[2] - 1;
-}
+#ifndef SEMLAB_PASS_YCOL
+#define SEMLAB_PASS_YCOL 1  // y passes of the (7,3) level by element columns (k_pass_ycol)
+#endif
 
-// One 1-D pass along AXIS. in/out are (x,y,z) arrays, x fastest, with local z offsets.
-// PROLONG: out[X] = sum_a J(i(X), a) in[e(X) qc + a]
-// RESTRICT: out[I] = sum over the 1-D support of coarse node I of J(i, a) in[X] (each X once)
-// The pass axis is a template parameter and the output coordinates come from 32-bit divisions
-// (the launcher checks the extents), so the index arithmetic stays off the critical path.
-// QF/QC > 0: the orders are compile-time constants (the (7,3,1) schedule), so the 1-D support
-// loops unroll and the element divisions become multiplications; 0: runtime orders.
-template <bool PROLONG, int AXIS, int QF, int QC>
+// The 1-D passes. PROLONG: out[X] = sum_a J(i(X), a) in[e(X) qc + a]; RESTRICT: out[I] = sum over
+// the 1-D support of coarse node I of J(i, a) in[X] (each X once: a coarse node shared by two
+// elements sums the left element, then the right one). Input masks zero the boundary sites of the
+// input lattice, output masks the boundary sites of the output; sub_from makes the input
+// (sub_from - in) (the residual b - A x fused into the first restriction pass); add_out adds the
+// result to out (x += P e fused into the last prolongation pass). Every weight is applied, zero or
+// not (w = 0 adds exactly +0), so the support's loads issue together. QF/QC > 0 are the
+// compile-time orders of the (7,3,1) schedule; 0: runtime orders.
+
+// y / z passes: one thread per output site, x along the threads, (y, z) from the block indices —
+// no divisions, and the row of J a block uses is uniform (a broadcast from the parameter bank).
+template <bool PROLONG, int AXIS, int QF, int QC, bool SUB>
 __global__ void __launch_bounds__(256) k_pass(const double* __restrict__ in, const Grid3 gin, double* __restrict__ out,
                                               const Grid3 gout, const Jmat J, const int qf_rt, const int qc_rt,
                                               const int E_axis, const int mask_in, const Grid3 gmask_in,
-                                              const int mask_out, const Grid3 gmask_out, const int zb, const int nz,
+                                              const int mask_out, const Grid3 gmask_out, const int zb,
                                               const int add_out, const double* __restrict__ sub_from) {
+  static_assert(AXIS == 1 || AXIS == 2, "k_pass: y or z");
   const int qf = QF > 0 ? QF : qf_rt, qc = QC > 0 ? QC : qc_rt;
-  const unsigned nx = unsigned(gout.N[0]), ny = unsigned(gout.N[1]);
-  const unsigned total = nx * ny * unsigned(nz);
-  const int jn = qc + 1;  // J is (qf+1) x (qc+1), row-major
-  const int64_t sin = AXIS == 0 ? 1 : (AXIS == 1 ? gin.nxl : gin.nxl * gin.nyl);
-  const int64_t nax_in = gmask_in.N[AXIS];
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const unsigned row = t / nx;
-    const int c[3] = {int(t - row * nx), int(row % ny), zb + int(row / ny)};
-    if (mask_out && gmask_out.dirichlet && on_boundary(c[0], c[1], c[2], gmask_out)) {
-      if (!add_out) out[gout.idx(c[0], c[1], c[2])] = 0.0;  // (add: out += 0)
-      continue;
+  const int jn = qc + 1;
+  const int x = int(blockIdx.x * blockDim.x + threadIdx.x);
+  if (x >= gout.N[0]) return;
+  const int y = int(blockIdx.y), z = zb + int(blockIdx.z);
+  double* o = out + gout.idx(x, y, z);
+  if (mask_out && gmask_out.dirichlet &&
+      (x == 0 || x == gmask_out.N[0] - 1 || y == 0 || y == gmask_out.N[1] - 1 || z == 0 || z == gmask_out.N[2] - 1)) {
+    if (!add_out) *o = 0.0;
+    return;
+  }
+  const bool min_ = mask_in && gmask_in.dirichlet;
+  const int oth = AXIS == 1 ? z : y;  // the coordinate that is neither x nor the pass axis
+  const bool other_bnd = min_ && (x == 0 || x == gmask_in.N[0] - 1 || oth == 0 || oth == gmask_in.N[AXIS == 1 ? 2 : 1] - 1);
+  const int nax_in = int(gmask_in.N[AXIS]);
+  const int64_t sin = AXIS == 1 ? gin.nxl : gin.nxl * gin.nyl;
+  const int64_t row_off = AXIS == 1 ? gin.idx(x, 0, z) : gin.idx(x, y, 0);  // + coord sin: global coord
+  const double* row_in = in + row_off;
+  const double* row_sub = SUB ? sub_from + row_off : nullptr;
+  auto fetch = [&](int coord) -> double {
+    const double a = __ldg(row_in + coord * sin);
+    double v = a;
+    if constexpr (SUB) v = __ldg(row_sub + coord * sin) - a;
+    return (min_ && (other_bnd || coord == 0 || coord == nax_in - 1)) ? 0.0 : v;
+  };
+  const int X = AXIS == 1 ? y : z;
+  double acc = 0.0;
+  if (PROLONG) {
+    int e = X / qf;
+    int i = X - e * qf;
+    if (e == E_axis) {
+      e -= 1;
+      i = qf;
     }
-    // input row through this point along AXIS; the other two coordinates fix the mask test
-    int c0[3] = {c[0], c[1], c[2]};
-    c0[AXIS] = 0;
-    const int64_t row_off = gin.idx(c0[0], c0[1], c0[2]);
-    const double* row_in = in + row_off;
-    const double* row_sub = sub_from ? sub_from + row_off : nullptr;
-    bool other_bnd = false;
-    if (mask_in && gmask_in.dirichlet) {
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-        if (d != AXIS) other_bnd = other_bnd || c[d] == 0 || c[d] == gmask_in.N[d] - 1;
-    }
-    const bool min_ = mask_in && gmask_in.dirichlet;
-    // branch-free: both loads always issue (coord is inside the lattice) and the mask selects, so
-    // the compiler can put the whole 1-D support's loads in flight together
-    const double* row_s = row_sub ? row_sub : row_in;
-    const bool has_sub = row_sub != nullptr;
-    auto fetch = [&](int coord) -> double {
-      const double a = __ldg(row_in + coord * sin), b = __ldg(row_s + coord * sin);
-      // sub_from: the input is (sub_from - in), e.g. the residual b - A x fused into Pᵀ
-      const double v = has_sub ? b - a : a;
-      return (min_ && (other_bnd || coord == 0 || coord == nax_in - 1)) ? 0.0 : v;
-    };
-    // every weight is applied, zero or not (w = 0 adds exactly +0): a branch on w would keep the
-    // compiler from issuing the support loads together, and the pass would be load-latency bound
-    const int X = c[AXIS];
-    double acc = 0.0;
-    if (PROLONG) {
-      int e = X / qf;
-      int i = X - e * qf;
-      if (e == E_axis) {
-        e -= 1;
-        i = qf;
-      }
+    if (i == 0 || i == qf) {
+      // a vertex site: its row of J is exactly the unit vector (lagrange_interpolation_matrix
+      // sets it on coinciding nodes), so the one nonzero term is the whole sum, bitwise — and
+      // a slab's top interface plane (e = ez1, i = 0) must not read past the slab's coarse planes
+      const int a = i == 0 ? 0 : qc;
+      acc += J.v[i * jn + a] * fetch(e * qc + a);
+    } else {
 #pragma unroll
       for (int a = 0; a < (QC > 0 ? QC + 1 : 16); ++a) {
         if (QC == 0 && a >= jn) break;
-        const double w = J.v[i * jn + a];
-        acc += w * fetch(e * qc + a);
+        acc += J.v[i * jn + a] * fetch(e * qc + a);
       }
-    } else {
-      const int I = X;
-      int e = I / qc;
-      const int a = I - e * qc;
-      if (a == 0 && e > 0) {  // shared coarse node: left element (a' = qc), then right element
-        // (on a slab, an element of the other rank contributes through the interface sum; the
-        // shared fine node X = e qf is counted with the left element only)
-        if (e - 1 >= J.e_lo)
-#pragma unroll
-          for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
-            if (QF == 0 && i > qf) break;
-            const double w = J.v[i * jn + qc];
-            acc += w * fetch((e - 1) * qf + i);
-          }
-        if (e < E_axis && e < J.e_hi)
-#pragma unroll
-          for (int i = 1; i < (QF > 0 ? QF + 1 : 16); ++i) {
-            if (QF == 0 && i > qf) break;
-            const double w = J.v[i * jn + 0];
-            acc += w * fetch(e * qf + i);
-          }
-      } else {
-        if (e == E_axis) e -= 1;  // last coarse node belongs to the last element
-        const int aa = I - e * qc;
+    }
+  } else {
+    int e = X / qc;
+    const int a = X - e * qc;
+    if (a == 0 && e > 0) {  // shared coarse node: left element (a' = qc), then right element
+      // (on a slab, an element of the other rank contributes through the interface sum; the
+      // shared fine node X = e qf is counted with the left element only)
+      if (e - 1 >= J.e_lo)
 #pragma unroll
         for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
           if (QF == 0 && i > qf) break;
-          const double w = J.v[i * jn + aa];
-          acc += w * fetch(e * qf + i);
+          acc += J.v[i * jn + qc] * fetch((e - 1) * qf + i);
         }
+      if (e < E_axis && e < J.e_hi)
+#pragma unroll
+        for (int i = 1; i < (QF > 0 ? QF + 1 : 16); ++i) {
+          if (QF == 0 && i > qf) break;
+          acc += J.v[i * jn + 0] * fetch(e * qf + i);
+        }
+    } else {
+      if (e == E_axis) e -= 1;  // last coarse node belongs to the last element
+      const int aa = X - e * qc;
+#pragma unroll
+      for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
+        if (QF == 0 && i > qf) break;
+        acc += J.v[i * jn + aa] * fetch(e * qf + i);
       }
     }
-    double* o = out + gout.idx(c[0], c[1], c[2]);
-    *o = add_out ? *o + acc : acc;  // add: the coarse correction x += P e fused into the last pass
+  }
+  *o = add_out ? *o + acc : acc;  // add: the coarse correction x += P e fused into the last pass
+}
+
+// The y pass for the compile-time orders: one thread per (x, element along y, z) forms all the
+// sites of its element column from one set of loads — prolongation: the qf sites of the element
+// from its qc+1 coarse values; restriction: the qc coarse nodes of the element from its qf+1 fine
+// values and those of the left element (the shared node). Same arithmetic and order as k_pass.
+template <bool PROLONG, int QF, int QC, bool SUB>
+__global__ void __launch_bounds__(256) k_pass_ycol(const double* __restrict__ in, const Grid3 gin,
+                                                   double* __restrict__ out, const Grid3 gout, const Jmat J,
+                                                   const int E_axis, const int mask_in, const Grid3 gmask_in,
+                                                   const int mask_out, const Grid3 gmask_out, const int zb,
+                                                   const int add_out, const double* __restrict__ sub_from) {
+  static_assert(QF > 0 && QC > 0, "k_pass_ycol: compile-time orders");
+  constexpr int jn = QC + 1;
+  const int x = int(blockIdx.x * blockDim.x + threadIdx.x);
+  if (x >= gout.N[0]) return;
+  const int e = int(blockIdx.y), z = zb + int(blockIdx.z);
+  const bool min_ = mask_in && gmask_in.dirichlet;
+  const bool other_bnd = min_ && (x == 0 || x == gmask_in.N[0] - 1 || z == 0 || z == gmask_in.N[2] - 1);
+  const int nax_in = int(gmask_in.N[1]);
+  const int64_t sin = gin.nxl;
+  const int64_t row_off = gin.idx(x, 0, z);
+  auto fetch = [&](int coord) -> double {
+    const double a = __ldg(in + row_off + coord * sin);
+    double v = a;
+    if constexpr (SUB) v = __ldg(sub_from + row_off + coord * sin) - a;
+    return (min_ && (other_bnd || coord == 0 || coord == nax_in - 1)) ? 0.0 : v;
+  };
+  const bool mout = mask_out && gmask_out.dirichlet;
+  const bool out_bnd = mout && (x == 0 || x == gmask_out.N[0] - 1 || z == 0 || z == gmask_out.N[2] - 1);
+  auto put = [&](int Y, double acc) {
+    double* o = out + gout.idx(x, Y, z);
+    if (mout && (out_bnd || Y == 0 || Y == gmask_out.N[1] - 1)) {
+      if (!add_out) *o = 0.0;
+      return;
+    }
+    *o = add_out ? *o + acc : acc;
+  };
+  if (PROLONG) {
+    double f[QC + 1];
+#pragma unroll
+    for (int a = 0; a <= QC; ++a) f[a] = fetch(e * QC + a);
+    const int ni = e == E_axis - 1 ? QF + 1 : QF;  // the last element also writes its far site
+#pragma unroll
+    for (int i = 0; i <= QF; ++i) {
+      if (i >= ni) break;
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a <= QC; ++a) acc += J.v[i * jn + a] * f[a];
+      put(e * QF + i, acc);
+    }
+  } else {
+    double f[QF + 1], fl[QF + 1];
+#pragma unroll
+    for (int i = 0; i <= QF; ++i) f[i] = fetch(e * QF + i);
+    if (e > 0) {
+#pragma unroll
+      for (int i = 0; i <= QF; ++i) fl[i] = fetch((e - 1) * QF + i);
+    }
+    {  // node e qc
+      double acc = 0.0;
+      if (e > 0) {
+        if (e - 1 >= J.e_lo)
+#pragma unroll
+          for (int i = 0; i <= QF; ++i) acc += J.v[i * jn + QC] * fl[i];
+        if (e < J.e_hi)
+#pragma unroll
+          for (int i = 1; i <= QF; ++i) acc += J.v[i * jn + 0] * f[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i <= QF; ++i) acc += J.v[i * jn + 0] * f[i];
+      }
+      put(e * QC, acc);
+    }
+#pragma unroll
+    for (int a = 1; a < QC; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i <= QF; ++i) acc += J.v[i * jn + a] * f[i];
+      put(e * QC + a, acc);
+    }
+    if (e == E_axis - 1) {  // the last coarse node E qc: the last element's local qc
+      double acc = 0.0;
+      if (e >= J.e_lo)
+#pragma unroll
+        for (int i = 0; i <= QF; ++i) acc += J.v[i * jn + QC] * f[i];
+      put(E_axis * QC, acc);
+    }
+  }
+}
+
+// The x pass: one block per (y, z) row, staged in shared memory. The input row is loaded
+// coalesced (masked, sub_from subtracted); the outputs are formed with the threads ordered
+// (local index, element) so a warp reads one row of J (a broadcast) and strided shared-memory
+// sites; they go to a shared output row and then to HBM coalesced (mask, add). Along x the
+// supports of neighbouring outputs overlap and the row of J differs per site, which made the
+// one-thread-per-site form latency- and replay-bound.
+template <bool PROLONG, int QF, int QC, bool SUB>
+__global__ void __launch_bounds__(1024) k_pass_x(const double* __restrict__ in, const Grid3 gin,
+                                                 double* __restrict__ out, const Grid3 gout, const Jmat J,
+                                                 const int qf_rt, const int qc_rt, const int E_axis,
+                                                 const int mask_in, const Grid3 gmask_in, const int mask_out,
+                                                 const Grid3 gmask_out, const int zb, const int nz, const int add_out,
+                                                 const double* __restrict__ sub_from) {
+  constexpr int RB = 4;  // rows per block step: each thread has RB independent loads per array in flight
+  extern __shared__ double sm[];
+  const int qf = QF > 0 ? QF : qf_rt, qc = QC > 0 ? QC : qc_rt;
+  const int jn = qc + 1;
+  const int nin = int(gin.N[0]), nout = int(gout.N[0]), ny = int(gout.N[1]);
+  double* srow = sm;             // RB input rows
+  double* sout = sm + RB * nin;  // RB output rows
+  const bool min_ = mask_in && gmask_in.dirichlet;
+  const bool mout = mask_out && gmask_out.dirichlet;
+  const int q_out = PROLONG ? qf : qc;  // sites per element on the output side
+  // one input site and one output site per thread (blockDim >= nin, nout): the site maps are
+  // computed once. Output t -> (l, e), l = t / E (uniform over most of a warp so the row of J is
+  // a broadcast), site X = e q_out + l; the last site E q_out last.
+  const int x = threadIdx.x;
+  const bool has_in = x < nin, has_out = x < nout;
+  const bool x_edge_in = x == 0 || x == gmask_in.N[0] - 1;
+  int l = x / E_axis, e = x - l * E_axis;
+  if (l == q_out) e = E_axis - 1;
+  const int X = e * q_out + l;
+  const bool x_edge_out = X == 0 || X == gmask_out.N[0] - 1;
+  {
+    // block (blockIdx.x, blockIdx.y) = rows y0 .. y0+RB-1 of plane z: no divisions, and the row
+    // bases are a stride apart
+    const int y0 = blockIdx.x * RB, z = zb + int(blockIdx.y);
+    const int64_t gi0 = gin.idx(0, y0, z), go0 = gout.idx(0, y0, z);
+    const bool zedge_in = z == 0 || z == gmask_in.N[2] - 1, zedge_out = z == 0 || z == gmask_out.N[2] - 1;
+    double vin[RB], vsub[RB], vout[RB];
+    int64_t gi[RB], go[RB];
+    bool edge_in[RB], edge_out[RB];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      const int y = min(y0 + rr, ny - 1);  // (a short last block repeats its last row; only nr are stored)
+      gi[rr] = gi0 + int64_t(y - y0) * gin.nxl;
+      go[rr] = go0 + int64_t(y - y0) * gout.nxl;
+      edge_in[rr] = zedge_in || y == 0 || y == gmask_in.N[1] - 1;
+      edge_out[rr] = zedge_out || y == 0 || y == gmask_out.N[1] - 1;
+      if (has_in) {
+        vin[rr] = __ldg(in + gi[rr] + x);
+        if constexpr (SUB) vsub[rr] = __ldg(sub_from + gi[rr] + x);
+      }
+      if (add_out && has_out) vout[rr] = out[go[rr] + X];
+    }
+    if (has_in) {
+#pragma unroll
+      for (int rr = 0; rr < RB; ++rr) {
+        double v = vin[rr];
+        if constexpr (SUB) v = vsub[rr] - v;
+        srow[rr * nin + x] = (min_ && (edge_in[rr] || x_edge_in)) ? 0.0 : v;
+      }
+    }
+    __syncthreads();
+    if (has_out) {
+#pragma unroll
+      for (int rr = 0; rr < RB; ++rr) {
+        const double* si = srow + rr * nin;
+        double acc = 0.0;
+        if (PROLONG) {
+#pragma unroll
+          for (int a = 0; a < (QC > 0 ? QC + 1 : 16); ++a) {
+            if (QC == 0 && a >= jn) break;
+            acc += J.v[l * jn + a] * si[e * qc + a];
+          }
+        } else if (l == 0 && e > 0) {  // shared coarse node e qc: left element, then right element
+          if (e - 1 >= J.e_lo)
+#pragma unroll
+            for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
+              if (QF == 0 && i > qf) break;
+              acc += J.v[i * jn + qc] * si[(e - 1) * qf + i];
+            }
+          if (e < J.e_hi)
+#pragma unroll
+            for (int i = 1; i < (QF > 0 ? QF + 1 : 16); ++i) {
+              if (QF == 0 && i > qf) break;
+              acc += J.v[i * jn + 0] * si[e * qf + i];
+            }
+        } else if (l == q_out) {  // the last coarse node E qc: the last element's local qc
+          if (e >= J.e_lo)
+#pragma unroll
+            for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
+              if (QF == 0 && i > qf) break;
+              acc += J.v[i * jn + qc] * si[e * qf + i];
+            }
+        } else {
+#pragma unroll
+          for (int i = 0; i < (QF > 0 ? QF + 1 : 16); ++i) {
+            if (QF == 0 && i > qf) break;
+            acc += J.v[i * jn + l] * si[e * qf + i];
+          }
+        }
+        const bool masked = mout && (edge_out[rr] || x_edge_out);
+        double v = add_out ? vout[rr] + acc : acc;
+        if (masked) v = add_out ? vout[rr] : 0.0;  // (add: out += 0)
+        sout[rr * nout + X] = v;
+      }
+    }
+    __syncthreads();
+    if (x < nout) {
+      const int nr = min(RB, ny - y0);
+#pragma unroll
+      for (int rr = 0; rr < RB; ++rr)
+        if (rr < nr) out[go[rr] + x] = sout[rr * nout + x];
+    }
   }
 }
 
@@ -137,22 +337,68 @@ int64_t launch_transfer_pass(bool prolong, const double* in, const Grid3& gin, d
   if (total >= (int64_t(1) << 32) || gmi.N[2] >= (int64_t(1) << 31) || zb >= (int64_t(1) << 31))
     invalid("transfer pass: lattice too large for 32-bit pass indexing");
   if (axis < 0 || axis > 2) invalid("transfer pass: axis must be 0, 1 or 2");
-#define L3_(PR, AX, QF, QC)                                                                                       \
-  k_pass<PR, AX, QF, QC><<<grid_for(total), 256, 0, s>>>(in, gin, out, gout, J, qf, qc, E_axis, mask_in, gmi, mask_out, \
-                                                          gmo, int(zb), int(nz), int(add_out), sub_from)
-#define L_(PR, AX)                                     \
-  do {                                                 \
-    if (qf == 7 && qc == 3) L3_(PR, AX, 7, 3);         \
-    else if (qf == 3 && qc == 1) L3_(PR, AX, 3, 1);    \
-    else L3_(PR, AX, 0, 0);                            \
+  if (gout.N[1] > 65535 || nz > 65535) invalid("transfer pass: more than 65535 rows along y or z");
+  if (axis == 0) {
+    const int64_t wid = std::max(gin.N[0], gout.N[0]);
+    const size_t smem = size_t(4) * size_t(gin.N[0] + gout.N[0]) * sizeof(double);
+    if (wid > 1024 || smem > 48 * 1024) invalid("transfer pass: x rows longer than 1024 sites");
+    if (gout.N[0] != (prolong ? int64_t(E_axis) * qf : int64_t(E_axis) * qc) + 1)
+      invalid("transfer pass: x extent does not match the element count");
+    const int block = int((wid + 31) / 32 * 32);
+    const dim3 grid(unsigned((gout.N[1] + 3) / 4), unsigned(nz));  // RB = 4 rows per block
+#define LX_(PR, QF, QC, SUB)                                                                                 \
+  k_pass_x<PR, QF, QC, SUB><<<grid, block, smem, s>>>(in, gin, out, gout, J, qf, qc, E_axis, mask_in, gmi,   \
+                                                      mask_out, gmo, int(zb), int(nz), int(add_out), sub_from)
+#define LXS_(PR, QF, QC) \
+  do {                   \
+    if (sub_from) LX_(PR, QF, QC, true); else LX_(PR, QF, QC, false); \
   } while (0)
-  if (prolong) {
-    if (axis == 0) L_(true, 0); else if (axis == 1) L_(true, 1); else L_(true, 2);
+#define LXQ_(PR)                                      \
+  do {                                                \
+    if (qf == 7 && qc == 3) LXS_(PR, 7, 3);           \
+    else if (qf == 3 && qc == 1) LXS_(PR, 3, 1);      \
+    else LXS_(PR, 0, 0);                              \
+  } while (0)
+    if (prolong) LXQ_(true); else LXQ_(false);
+#undef LXQ_
+#undef LXS_
+#undef LX_
   } else {
-    if (axis == 0) L_(false, 0); else if (axis == 1) L_(false, 1); else L_(false, 2);
+    const unsigned bx = unsigned(std::min<int64_t>(256, (gout.N[0] + 31) / 32 * 32));
+    const dim3 grid(unsigned((gout.N[0] + bx - 1) / bx), unsigned(gout.N[1]), unsigned(nz));
+#define LP_(PR, AX, QF, QC, SUB)                                                                            \
+  k_pass<PR, AX, QF, QC, SUB><<<grid, bx, 0, s>>>(in, gin, out, gout, J, qf, qc, E_axis, mask_in, gmi,     \
+                                                 mask_out, gmo, int(zb), int(add_out), sub_from)
+#define LPS_(PR, AX, QF, QC) \
+  do {                       \
+    if (sub_from) LP_(PR, AX, QF, QC, true); else LP_(PR, AX, QF, QC, false); \
+  } while (0)
+#define LPQ_(PR, AX)                                  \
+  do {                                                \
+    if (qf == 7 && qc == 3) LPS_(PR, AX, 7, 3);       \
+    else if (qf == 3 && qc == 1) LPS_(PR, AX, 3, 1);  \
+    else LPS_(PR, AX, 0, 0);                          \
+  } while (0)
+    if (axis == 1 && qf == 7 && qc == 3 && SEMLAB_PASS_YCOL) {
+      if (gout.N[1] != (prolong ? int64_t(E_axis) * qf : int64_t(E_axis) * qc) + 1)
+        invalid("transfer pass: y extent does not match the element count");
+      const dim3 gcol(grid.x, unsigned(E_axis), unsigned(nz));
+#define LC_(PR, SUB)                                                                                        \
+  k_pass_ycol<PR, 7, 3, SUB><<<gcol, bx, 0, s>>>(in, gin, out, gout, J, E_axis, mask_in, gmi, mask_out, gmo, \
+                                                 int(zb), int(add_out), sub_from)
+      if (prolong) LC_(true, false);
+      else if (sub_from) LC_(false, true);
+      else LC_(false, false);
+#undef LC_
+    } else if (prolong) {
+      if (axis == 1) LPQ_(true, 1); else LPQ_(true, 2);
+    } else {
+      if (axis == 1) LPQ_(false, 1); else LPQ_(false, 2);
+    }
+#undef LPQ_
+#undef LPS_
+#undef LP_
   }
-#undef L_
-#undef L3_
   SB_LAUNCH_CHECK();
   return 1;
 }
