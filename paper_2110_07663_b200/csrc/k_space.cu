@@ -989,6 +989,41 @@ __device__ __forceinline__ Cand2 cand2(int c, int q, int lo_e, int hi_e) {
   return r;
 }
 
+// The split-path gather (low orders): one thread per lattice node of the slab, x along the
+// threads and (y, z) from the block indices (32-bit, no divisions by runtime extents); the node
+// sums its <= 8 contributors' element-local values in ascending element id (z, then y, then x
+// candidates, lower first — sem_space.cpp:110-119), loads predicated and issued together; absent
+// contributors add +0.0, so the sums are bitwise those of the candidate-list loops.
+template <int ND, class EpiT>
+__global__ void __launch_bounds__(128) k_gather_epi(const Slab sl, const double* __restrict__ loc, const EpiT epi) {
+  constexpr int q = ND - 1, NLOC = ND * ND * ND;
+  const int x = int(blockIdx.x * blockDim.x + threadIdx.x);
+  if (x >= sl.Nx) return;
+  const int y = int(blockIdx.y), z = sl.ez0 * q + int(blockIdx.z);
+  const int64_t g = sl.lidx(x, y, z);
+  if (sl.masked(x, y, z)) {
+    epi(g, 0.0);
+    return;
+  }
+  const Cand2 cx = cand2(x, q, 0, sl.Ex), cy = cand2(y, q, 0, sl.Ey), cz = cand2(z, q, sl.ez0, sl.ez1);
+  double v[8];
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const bool on = (c ? cz.v1 : cz.v0) && (b ? cy.v1 : cy.v0) && (a ? cx.v1 : cx.v0);
+        const int el = (a ? cx.e1 : cx.e0) + sl.Ex * ((b ? cy.e1 : cy.e0) + sl.Ey * ((c ? cz.e1 : cz.e0) - sl.ez0));
+        const int li = (a ? cx.l1 : cx.l0) + ND * ((b ? cy.l1 : cy.l0) + ND * (c ? cz.l1 : cz.l0));
+        v[c * 4 + b * 2 + a] = on ? __ldg(loc + int64_t(el) * NLOC + li) : 0.0;
+      }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc += v[k];
+  epi(g, acc);
+}
+
 // One face lattice node (x, y, z) of family FAM: sum its contributors' face-buffer entries in
 // ascending element id — the (lower, upper) candidates of z, then y, then x, the loads predicated
 // and issued together — apply the Dirichlet mask and the epilogue. The family fixes which axes
@@ -1122,31 +1157,6 @@ constexpr bool ax_dmma() { return SEMLAB_AX_DMMA != 0; }
 
 // Q^T of element-local results with an owner epilogue: each lattice node sums its <= 8
 // contributors in ascending element id (sem_space.cpp:110-119 order), masked nodes get 0.
-template <int ND, class EpiT>
-__global__ void __launch_bounds__(256) k_gather_epi(const Slab sl, const double* __restrict__ loc, const EpiT epi) {
-  constexpr int q = ND - 1, NLOC = ND * ND * ND;
-  const int64_t zb = int64_t(sl.ez0) * q, nz = int64_t(sl.ez1 - sl.ez0) * q + 1;
-  const int64_t total = sl.Nx * sl.Ny * nz;
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t x = t % sl.Nx, y = (t / sl.Nx) % sl.Ny, z = zb + t / (sl.Nx * sl.Ny);
-    const int64_t g = sl.lidx(x, y, z);
-    if (sl.masked(x, y, z)) {
-      epi(g, 0.0);
-      continue;
-    }
-    const Cands cx = cands(x, q, sl.Ex, 0, sl.Ex), cy = cands(y, q, sl.Ey, 0, sl.Ey);
-    const Cands cz = cands(z, q, sl.Ez, sl.ez0, sl.ez1);
-    double acc = 0.0;
-    for (int c = 0; c < cz.n; ++c)
-      for (int b = 0; b < cy.n; ++b)
-        for (int a = 0; a < cx.n; ++a) {
-          const int64_t el = cx.e[a] + int64_t(sl.Ex) * (cy.e[b] + int64_t(sl.Ey) * (cz.e[c] - sl.ez0));
-          acc += loc[el * NLOC + cx.loc[a] + ND * (cy.loc[b] + ND * cz.loc[c])];
-        }
-    epi(g, acc);
-  }
-}
-
 template <int ND, bool LOCAL, class EpiT>
 int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, const AxSync& sy, double* out_local,
                        const EpiT& epi, cudaStream_t s) {
@@ -1171,8 +1181,11 @@ int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, cons
                                            IO == 2 ? sy.dep : out_local, epi);
   SB_LAUNCH_CHECK();
   if constexpr (IO == 2) {
-    const int64_t total = sl.Nx * sl.Ny * (int64_t(sl.ez1 - sl.ez0) * sl.q + 1);
-    k_gather_epi<ND><<<grid1d(total, 256), 256, 0, s>>>(sl, sy.dep, epi);
+    const int64_t nzl = int64_t(sl.ez1 - sl.ez0) * sl.q + 1;
+    if (sl.Ny > 65535 || nzl > 65535 || nE * NLOC >= (int64_t(1) << 31))
+      invalid("SemSpace: lattice too large for the split-path gather");
+    k_gather_epi<ND><<<dim3(unsigned((sl.Nx + 127) / 128), unsigned(sl.Ny), unsigned(nzl)), 128, 0, s>>>(sl, sy.dep,
+                                                                                                         epi);
     SB_LAUNCH_CHECK();
     return 2;
   }
