@@ -150,7 +150,7 @@ int semlab_space_sizes(semlab_space s, int64_t out[11]);
 /* apply_A, sem_space.cpp:195-209: out = mask o Q^T A_L Q o mask (in). */
 int semlab_space_apply_A(semlab_space s, const double* d_in, double* d_out);
 /* Extension (no reference analogue): apply_A with the geometric factors rounded to FP32 and FP64
-   arithmetic, the operator of the FP32 smoother (order 7 only; EINVAL otherwise). */
+   arithmetic, the operator of the FP32 smoother (orders 7 and <= 5; EINVAL otherwise). */
 int semlab_space_apply_A_geom32(semlab_space s, const double* d_in, double* d_out);
 /* apply_local_stiffness on every element (E-vector in/out), sem_space.cpp:127-180. */
 int semlab_space_apply_local_stiffness(semlab_space s, const double* d_local_in, double* d_local_out);

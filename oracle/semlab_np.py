@@ -353,8 +353,8 @@ class SemSpace:
 
     def with_geom32(self):
         """A view of this space whose geometric factors are rounded to FP32 (arithmetic stays
-        FP64): the operator the B200 product's FP32 smoother applies at order 7 (its pMG levels'
-        smoother A, lambda estimate and V-cycle residual). Not a reference function: the reference
+        FP64): the operator the B200 product's FP32 smoother applies at orders 7 and <= 5 (its pMG
+        levels' smoother A, lambda estimate and V-cycle residual). Not a reference function: the reference
         has no FP32 smoother; this pins that product variant to FP64-arithmetic ground truth."""
         import copy
         c = copy.copy(self)
@@ -1148,9 +1148,11 @@ class Pmg:
         self.spaces = [SemSpace(mesh, q, bc) for q in orders]
         self.levels = []
         for sp_ in self.spaces[:-1]:
-            # precision 32 at order 7: the smoother's operator uses FP32-rounded factors, like the
-            # product (pmg.cpp build(): L.A->geom32); the Krylov operator is not part of Pmg
-            A = sp_.with_geom32().apply_A if (precision == 32 and sp_.order == 7) else sp_.apply_A
+            # precision 32: every smoothed level's operator uses FP32-rounded factors, like the
+            # product (pmg.cpp build(): L.A->geom32, orders 7 and <= 5); the Krylov operator is
+            # not part of Pmg
+            A = sp_.with_geom32().apply_A if (precision == 32 and (sp_.order == 7 or sp_.order <= 5)) \
+                else sp_.apply_A
             if smoother == "jacobi":
                 inv = jacobi_inverse_diag(sp_)
                 S = (lambda inv: (lambda v: inv * v))(inv)

@@ -305,7 +305,7 @@ int semlab_space_apply_A(semlab_space s, const double* in, double* out) {
 int semlab_space_apply_A_geom32(semlab_space s, const double* in, double* out) {
   return guard([&] {
     need(s, "apply_A_geom32: space");
-    if (!s->enable_geom32()) invalid("apply_A_geom32: FP32 geometric factors exist for order 7 only");
+    if (!s->enable_geom32()) invalid("apply_A_geom32: FP32 geometric factors exist for orders 7 and <= 5 only");
     s->apply_A(in, out, true);
   });
 }
@@ -427,7 +427,7 @@ int semlab_op_A(semlab_space s, semlab_op* out) {
 int semlab_op_A_geom32(semlab_space s, semlab_op* out) {
   return guard([&] {
     need(s, "semlab_op_A_geom32: space");
-    if (!s->enable_geom32()) invalid("semlab_op_A_geom32: FP32 geometric factors exist for order 7 only");
+    if (!s->enable_geom32()) invalid("semlab_op_A_geom32: FP32 geometric factors exist for orders 7 and <= 5 only");
     auto o = std::make_unique<semlab_op_s>();
     o->kind = semlab_op_s::kA;
     o->ctx = s->ctx;

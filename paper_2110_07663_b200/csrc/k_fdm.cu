@@ -33,7 +33,7 @@ constexpr int kGatherUnroll = SEMLAB_RASW_GATHER_UNROLL;
 #endif
 
 #ifndef SEMLAB_RAS_SMALLP_MINB
-#define SEMLAB_RAS_SMALLP_MINB 5  // p = 3 level (P = 6): 5 CTAs/SM of the CTA RAS kernel
+#define SEMLAB_RAS_SMALLP_MINB 7  // p = 3 level (P = 6): 7 CTAs/SM of the CTA RAS kernel (3% faster than 5 despite 12 B of spills)
 #endif
 #ifndef SEMLAB_RASW_MINP
 #define SEMLAB_RASW_MINP 8  // warp-per-element RAS from box size P = p + 3 >= this (p >= 3)
@@ -115,7 +115,19 @@ __device__ __forceinline__ void line_pass(const T* __restrict__ src, T* __restri
       for (int o = 0; o < P; ++o) y[r][o] = T(0);
 #pragma unroll
     for (int a = 0; a < P; ++a) {
-      if constexpr (P % 2 == 0) {
+      if constexpr (P % 2 == 0 && sizeof(T) == 4 && SEMLAB_RASW_FFMA2) {
+        // packed FP32 (FFMA2): the (o, o+1) output pair shares x_a; same per-output order
+#pragma unroll
+        for (int o = 0; o < P; o += 2) {
+          const float2 s2 = *reinterpret_cast<const float2*>(M + a * P + o);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const float2 acc = __ffma2_rn(s2, make_float2(x[r][a], x[r][a]), make_float2(y[r][o], y[r][o + 1]));
+            y[r][o] = acc.x;
+            y[r][o + 1] = acc.y;
+          }
+        }
+      } else if constexpr (P % 2 == 0) {
 #pragma unroll
         for (int o = 0; o < P; o += 2) {
           T s0, s1;
@@ -151,7 +163,21 @@ __device__ __forceinline__ void line_pass(const T* __restrict__ src, T* __restri
       for (int a = 0; a < P; ++a) y[r][a] = T(0);
 #pragma unroll
     for (int a = 0; a < P; ++a) {
-      if constexpr (P % 2 == 0) {
+      if constexpr (P % 2 == 0 && sizeof(T) == 4 && SEMLAB_RASW_FFMA2) {
+        // packed FP32: even and odd o accumulate in the two halves, summed at the end (the
+        // order of k_rasw's backward pass)
+        float2 a2[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) a2[r] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int o = 0; o < P; o += 2) {
+          const float2 s2 = *reinterpret_cast<const float2*>(M + a * P + o);
+#pragma unroll
+          for (int r = 0; r < R; ++r) a2[r] = __ffma2_rn(s2, make_float2(x[r][o], x[r][o + 1]), a2[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) y[r][a] = a2[r].x + a2[r].y;
+      } else if constexpr (P % 2 == 0) {
 #pragma unroll
         for (int o = 0; o < P; o += 2) {
           T s0, s1;

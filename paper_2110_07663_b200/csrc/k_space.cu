@@ -17,6 +17,7 @@
 //   * the owner applies an epilogue (plain write, residual, or a whole Chebyshev-Jacobi
 //     vector update) so the smoother needs no extra pass over the vectors.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "device.cuh"
@@ -187,9 +188,11 @@ constexpr int ax_min_blocks() {  // occupancy target: caps registers so ~20 warp
 
 // IO: 0 global -> global with the owner-ordered Q^T; 1 local -> local (E-vectors); 2 global in,
 // element-local out (the split path: k_gather_epi then sums in the reference order)
-template <int ND, int EPB, int IO, class EpiT>
+// GT: the geometric-factor storage type (double; float = the FP32 smoother's FP32-rounded factors,
+// FP64 arithmetic)
+template <int ND, int EPB, int IO, class EpiT, class GT = double>
 __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
-    k_ax(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const double* __restrict__ geom,
+    k_ax(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const GT* __restrict__ geom,
          double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int ngroups,
          double* __restrict__ out_local, const EpiT epi) {
   constexpr int ND2 = ND * ND, NLOC = ND2 * ND, NT = EPB * ND2;
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
   {  // stream the group's geometry (contiguous, 48 B/node) into L2 while u is loaded and
      // differentiated; phase 2 then reads it at L2 latency without holding shared memory
     const char* gbase = reinterpret_cast<const char*>(geom + e0 * 6 * NLOC);
-    const int lines = (ne * 6 * NLOC * int(sizeof(double)) + 127) / 128;
+    const int lines = (ne * 6 * NLOC * int(sizeof(GT)) + 127) / 128;
     for (int l = tid; l < lines; l += NT) asm volatile("prefetch.global.L2 [%0];" ::"l"(gbase + size_t(l) * 128));
   }
   if (tid == 0 && IO == 0) s_epoch = *reinterpret_cast<volatile unsigned*>(&flags[e0]);
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
   }
 
   // phase 2: geometric factors (sem_space.cpp:153-161), read from L2 (prefetched above)
-  const double* gg = geom + el * 6 * NLOC + ij;
+  const GT* gg = geom + el * 6 * NLOC + ij;
 #pragma unroll
   for (int k = 0; k < ND; ++k) {
     // per-layer guarded loads: keeps the 6*ND geometry loads from all being hoisted at once
@@ -279,12 +282,12 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
     const int node = k * ND2;
     double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0;
     if (active) {
-      g0 = __ldcs(gg + 0 * NLOC + node);
-      g1 = __ldcs(gg + 1 * NLOC + node);
-      g2 = __ldcs(gg + 2 * NLOC + node);
-      g3 = __ldcs(gg + 3 * NLOC + node);
-      g4 = __ldcs(gg + 4 * NLOC + node);
-      g5 = __ldcs(gg + 5 * NLOC + node);
+      g0 = double(__ldcs(gg + 0 * NLOC + node));
+      g1 = double(__ldcs(gg + 1 * NLOC + node));
+      g2 = double(__ldcs(gg + 2 * NLOC + node));
+      g3 = double(__ldcs(gg + 3 * NLOC + node));
+      g4 = double(__ldcs(gg + 4 * NLOC + node));
+      g5 = double(__ldcs(gg + 5 * NLOC + node));
     }
     const double r = ur[k], s = us[k], t = ut[k];
     ur[k] = g0 * r + g1 * s + g2 * t;
@@ -1157,10 +1160,10 @@ constexpr bool ax_dmma() { return SEMLAB_AX_DMMA != 0; }
 
 // Q^T of element-local results with an owner epilogue: each lattice node sums its <= 8
 // contributors in ascending element id (sem_space.cpp:110-119 order), masked nodes get 0.
-template <int ND, bool LOCAL, class EpiT>
-int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, const AxSync& sy, double* out_local,
+template <int ND, bool LOCAL, class EpiT, class GT = double>
+int64_t ax_dispatch_nd(const Slab& sl, const double* u, const GT* geom, const AxSync& sy, double* out_local,
                        const EpiT& epi, cudaStream_t s) {
-  if constexpr (!LOCAL && ND >= 8) {
+  if constexpr (!LOCAL && ND >= 8 && std::is_same_v<GT, double>) {
     if constexpr (ND == 8) {
       if (ax_dmma()) return axw_launch(sl, u, geom, sy, epi, s);
     }
@@ -1175,7 +1178,8 @@ int64_t ax_dispatch_nd(const Slab& sl, const double* u, const double* geom, cons
   // low orders: element-local Ax into the deposit buffer, then the ordered gather with the
   // epilogue (two fully parallel launches instead of CTAs idling on neighbour counters)
   constexpr int IO = LOCAL ? 1 : (ND <= SEMLAB_AX_SPLIT_ND ? 2 : 0);
-  auto kern = k_ax<ND, EPB, IO, EpiT>;
+  static_assert(std::is_same_v<GT, double> || IO == 2, "FP32 factors: the split path only");
+  auto kern = k_ax<ND, EPB, IO, EpiT, GT>;
   smem_attr(kern, smem);
   kern<<<ngroups, EPB * ND * ND, smem, s>>>(sl, dmat<ND>(sl.q), u, geom, sy.dep, sy.flags, sy.ticket, ngroups,
                                            IO == 2 ? sy.dep : out_local, epi);
@@ -1404,9 +1408,36 @@ int64_t launch_ax(const Slab& sl, const double* u, const double* geom, const AxS
   return 0;
 }
 
+template <int ND>
+int64_t ax_g32_split(const Slab& sl, const double* u, const float* g, const AxSync& sy, Epi epi, const EpiArgs& a,
+                     cudaStream_t s) {
+  switch (epi) {
+    case Epi::Write: return ax_dispatch_nd<ND, false>(sl, u, g, sy, nullptr, EWrite{a.w}, s);
+    case Epi::Residual: return ax_dispatch_nd<ND, false>(sl, u, g, sy, nullptr, EResidual{a.w, a.b}, s);
+    case Epi::ChebJacStep:
+      return ax_dispatch_nd<ND, false>(sl, u, g, sy, nullptr, EChebJacStep{a.x, a.r, a.d, a.inv, a.c1, a.c2}, s);
+    case Epi::ChebJacInit:
+      return ax_dispatch_nd<ND, false>(sl, u, g, sy, nullptr, EChebJacInit{a.r, a.d, a.b, a.inv, a.c1}, s);
+  }
+  return 0;
+}
+
+bool ax_g32_supported(int q) { return q == 7 || (q >= 1 && q + 1 <= SEMLAB_AX_SPLIT_ND); }
+
 int64_t launch_ax_g32(const Slab& sl, const double* u, const float* geom32, const AxSync& sy, Epi epi,
                       const EpiArgs& a, cudaStream_t s) {
-  if (sl.q != 7) invalid("launch_ax_g32: FP32 geometry is implemented for order 7");
+  if (!ax_g32_supported(sl.q))
+    invalid("launch_ax_g32: FP32 geometry is implemented for order 7 and the split-path orders");
+  if (sl.q != 7) {
+    switch (sl.q + 1) {
+      case 2: return ax_g32_split<2>(sl, u, geom32, sy, epi, a, s);
+      case 3: return ax_g32_split<3>(sl, u, geom32, sy, epi, a, s);
+      case 4: return ax_g32_split<4>(sl, u, geom32, sy, epi, a, s);
+      case 5: return ax_g32_split<5>(sl, u, geom32, sy, epi, a, s);
+      case 6: return ax_g32_split<6>(sl, u, geom32, sy, epi, a, s);
+      default: invalid("launch_ax_g32: unsupported order");
+    }
+  }
   switch (epi) {
     case Epi::Write: return axw_launch(sl, u, geom32, sy, EWrite{a.w}, s);
     case Epi::Residual: return axw_launch(sl, u, geom32, sy, EResidual{a.w, a.b}, s);

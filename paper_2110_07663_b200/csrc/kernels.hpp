@@ -38,6 +38,8 @@ int64_t launch_geom(const Slab& sl, const double* d_X, double* d_geom, double* d
 int64_t launch_ax(const Slab& sl, const double* d_u, const double* d_geom, const AxSync& sync, Epi epi,
                   const EpiArgs& a, cudaStream_t s);
 // Same operator with FP32-rounded geometric factors (order 7 only): the smoother's A.
+// orders with an FP32-factor Ax: 7 (k_axe) and the split-path orders (k_ax + k_gather_epi)
+bool ax_g32_supported(int q);
 int64_t launch_ax_g32(const Slab& sl, const double* d_u, const float* d_geom32, const AxSync& sync, Epi epi,
                       const EpiArgs& a, cudaStream_t s);
 int64_t launch_to_f32(const double* in, float* out, int64_t n, cudaStream_t s);

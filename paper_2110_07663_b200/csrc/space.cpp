@@ -329,7 +329,7 @@ void semlab_space_s::ax(const double* in, Epi epi, const EpiArgs& a, bool g32) {
 }
 
 bool semlab_space_s::enable_geom32() {
-  if (order != 7) return false;
+  if (!ax_g32_supported(order)) return false;
   if (!has_geom32()) {
     geom32.alloc(size_t(E) * 6 * size_t(nloc));
     ctx->count(launch_to_f32(geom.p, geom32.p, E * 6 * nloc, ctx->stream));

@@ -248,7 +248,8 @@ class SemSpace:
         return out
 
     def apply_A_geom32(self, u, out: torch.Tensor | None = None) -> torch.Tensor:
-        """apply_A with FP32-rounded geometric factors (the FP32 smoother's operator, order 7)."""
+        """apply_A with FP32-rounded geometric factors (the FP32 smoother's operator; order 7 and
+        orders <= 5)."""
         u = self.to_device(u)
         out = self.zeros() if out is None else out
         check(lib.semlab_space_apply_A_geom32(self.handle, _ptr(u), _ptr(out)))
@@ -314,7 +315,7 @@ class SemSpace:
         return LinOp(h, self.n, self.ctx, keep=self)
 
     def as_linop_geom32(self) -> LinOp:
-        """apply_A_geom32 as an operator: the FP32 smoother's A (order 7)."""
+        """apply_A_geom32 as an operator: the FP32 smoother's A (order 7 and orders <= 5)."""
         h = C.c_void_p()
         check(lib.semlab_op_A_geom32(self.handle, C.byref(h)))
         return LinOp(h, self.n, self.ctx, keep=self)

@@ -49,10 +49,13 @@ def test_ax_grid_cap_bitwise(ctx, eps, E, p):
     assert rel(full, want) < 1e-12
 
 
-def test_ax_geom32_grid_cap_and_oracle(ctx):
+@pytest.mark.parametrize("p", [7, 3, 5])
+def test_ax_geom32_grid_cap_and_oracle(ctx, p):
+    """FP32-rounded factors, FP64 arithmetic: order 7 (k_axe) and the split-path orders (k_ax +
+    k_gather_epi, the p=3 pMG level) against the oracle with the same rounded factors."""
     from paper_2110_07663_b200 import semlab as S
-    sp = S.SemSpace(S.generate_kershaw(0.3, 6, ctx), 7)
-    cs = o.SemSpace(o.generate_kershaw(0.3, 6), 7)
+    sp = S.SemSpace(S.generate_kershaw(0.3, 6, ctx), p)
+    cs = o.SemSpace(o.generate_kershaw(0.3, 6), p)
     u = np.random.default_rng(5).standard_normal(sp.n)
     full = sp.apply_A_geom32(u)
     with grid_cap(1):
