@@ -774,17 +774,29 @@ __device__ __forceinline__ int face_idx(int i, int j, int k) {
 #ifndef SEMLAB_AXW_WARPS
 #define SEMLAB_AXW_WARPS 4  // warps (independent element pipelines) per CTA
 #endif
+#ifndef SEMLAB_AXW_GEOM_AHEAD
+#define SEMLAB_AXW_GEOM_AHEAD 1  // FP32-factor layers loaded ahead of the one in use (2, 3 measured slower)
+#endif
 #ifndef SEMLAB_AXW_MINB
 #define SEMLAB_AXW_MINB 3  // resident CTAs per SM
 #endif
 
 __host__ __device__ constexpr int axw_warp_doubles() { return 3 * axw::ARR; }  // per-warp shared memory in doubles
 
-__device__ __forceinline__ double2 ld_geom2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
-__device__ __forceinline__ double2 ld_geom2(const float* p) {
-  const float2 v = __ldcs(reinterpret_cast<const float2*>(p));
-  return make_double2(double(v.x), double(v.y));
-}
+template <class GT>
+struct GeomRaw;
+template <>
+struct GeomRaw<double> {
+  using T = double2;
+};
+template <>
+struct GeomRaw<float> {
+  using T = float2;
+};
+__device__ __forceinline__ double2 ld_geom_raw(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ float2 ld_geom_raw(const float* p) { return __ldcs(reinterpret_cast<const float2*>(p)); }
+__device__ __forceinline__ double2 geom_to_d2(double2 v) { return v; }
+__device__ __forceinline__ double2 geom_to_d2(float2 v) { return make_double2(double(v.x), double(v.y)); }
 
 // GT = double: the operator itself (Krylov A). GT = float: the smoother's operator with the
 // geometric factors rounded to FP32 (half the bytes; arithmetic stays FP64 on the DMMA path).
@@ -869,17 +881,23 @@ __global__ void __launch_bounds__(32 * SEMLAB_AXW_WARPS, SEMLAB_AXW_MINB)
     __syncwarp();
     // per z-layer: ur, us (DMMA), ut (workspace), geometric factors, then Gr/Gs/Gt back out
     const GT* ge = geom + size_t(el) * 6 * NLOC + j * ND + i0;
-    double2 gA[6], gB[6];
+    // geometry ring: GD layers in flight ahead of the one in use (FP32 factors stay packed in
+    // registers until used, so the deeper ring costs fewer registers than FP64's one-ahead)
+    constexpr int GD = std::is_same_v<GT, float> ? SEMLAB_AXW_GEOM_AHEAD : 1;
+    typename GeomRaw<GT>::T gq[GD + 1][6];
 #pragma unroll
-    for (int c = 0; c < 6; ++c) gA[c] = ld_geom2(ge + c * NLOC);
+    for (int a = 0; a < GD; ++a)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) gq[a][c] = ld_geom_raw(ge + c * NLOC + a * ND2);
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
-      double2* gcur = (k & 1) ? gB : gA;
-      double2* gnext = (k & 1) ? gA : gB;
-      if (k + 1 < ND) {
+      if (k + GD < ND) {
 #pragma unroll
-        for (int c = 0; c < 6; ++c) gnext[c] = ld_geom2(ge + c * NLOC + (k + 1) * ND2);
+        for (int c = 0; c < 6; ++c) gq[(k + GD) % (GD + 1)][c] = ld_geom_raw(ge + c * NLOC + (k + GD) * ND2);
       }
+      double2 gcur[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) gcur[c] = geom_to_d2(gq[k % (GD + 1)][c]);
       double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int kc = 0; kc < 2; ++kc) {
