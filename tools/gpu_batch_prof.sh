@@ -2,7 +2,7 @@
 # 1-GPU profiling batch: Ax variant A/B, ncu --set full of the roofline kernels (traffic), tests, bench.
 T=${1:-prof}
 mkdir -p gpurun_out
-for v in "" axw_minb4; do
+for v in ""; do
   if [ -z "$v" ]; then lib=libsemlab_b200.so; else lib=libsemlab_b200_$v.so; fi
   SEMLAB_LIB=$lib timeout 300 python tools/perf_probe.py --solve 1 > gpurun_out/${T}_probe_${v:-default}.log 2>&1
 done
