@@ -513,8 +513,9 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=0,
                     help="iterations of the reference timed for cpu_baseline after its setup (0: sized to the mesh)")
     ap.add_argument("--no-fp64-line", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
-                    help="z-slab plane exchanges: NCCL send/recv or NVLink peer-memory mail slots")
+    ap.add_argument("--exchange", default="peer", choices=["nccl", "peer"],
+                    help="z-slab plane exchanges: NVLink peer-memory mail slots (default; falls back to "
+                         "NCCL when a rank cannot map its neighbours) or NCCL send/recv")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("timing rules: --warmup must be >= 3")
