@@ -38,9 +38,6 @@ constexpr int kGatherUnroll = SEMLAB_RASW_GATHER_UNROLL;
 #ifndef SEMLAB_RASW_MINP
 #define SEMLAB_RASW_MINP 8  // warp-per-element RAS from box size P = p + 3 >= this (p >= 3)
 #endif
-#ifndef SEMLAB_RASW_EPI_PF
-#define SEMLAB_RASW_EPI_PF 1  // prefetch the Chebyshev-step owner write's x, r, d rows to L2
-#endif
 #ifndef SEMLAB_RASW_FFMA2
 #define SEMLAB_RASW_FFMA2 1  // packed FP32 FMA (sm_100 FFMA2) in the FDM line passes
 #endif
@@ -587,21 +584,6 @@ __global__ void __launch_bounds__(WShape<P, T>::NT, sizeof(T) == 4 ? SEMLAB_RASW
       }
     }
 #endif
-    if constexpr (MODE >= 2 && SEMLAB_RASW_EPI_PF) {
-      // the Chebyshev step's owner write reads x, r and d at the owned sites: start those rows
-      // towards L2 now, so the write does not wait on HBM latency once per round
-      const int nb = Y.own_hi - Y.own_lo + 1, nc = Z.own_hi - Z.own_lo + 1, na = X.own_hi - X.own_lo + 1;
-      for (int rw = lane; rw < nb * nc; rw += 32) {
-        const int64_t g = sl.lidx(X.lo + X.own_lo, Y.lo + Y.own_lo + rw % nb, Z.lo + Z.own_lo + rw / nb);
-        const double* vs[3] = {epi.x, epi.r, epi.d};
-#pragma unroll
-        for (int v = 0; v < 3; ++v) {
-          const double* p = vs[v] + g;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p + na - 1));
-        }
-      }
-    }
     __syncwarp();  // the previous element's owner write has finished reading tmp
     {  // factors: S (3 P^2) and lambda (3 P), all loads issued before the stores
       constexpr int NF = 3 * P2 + 3 * P, IT = (NF + 31) / 32;

@@ -1051,18 +1051,31 @@ __global__ void __launch_bounds__(128) k_gather_epi(const Slab sl, const double*
 // can split (FAM 0: z on an element face, x and y any; FAM 1: z interior, y on a face, x any;
 // FAM 2: z and y interior, x on a face), so only the 8 / 4 / 2 possible contributors are formed
 // and their face indices reduce to the closed forms of face_idx for that face.
+// A face lattice node in flight: its contributors' face-buffer values (absent ones +0.0, padded
+// to 8), its lattice index, the Dirichlet mask and the epilogue's inputs.
+template <class EpiT>
+struct FaceSite {
+  double v[8];
+  int64_t g;
+  bool on, masked;
+  typename EpiT::In in;
+};
+
+// Issue the loads of face node (x, y, z) of family FAM: its contributors' face-buffer entries in
+// ascending element id — the (lower, upper) candidates of z, then y, then x — all predicated and
+// issued together. The family fixes which axes can split (FAM 0: z on an element face, x and y
+// any; FAM 1: z interior, y on a face, x any; FAM 2: z and y interior, x on a face), so only the
+// 8 / 4 / 2 possible contributors are formed and their face indices reduce to closed forms.
 template <int FAM, class EpiT>
-__device__ __forceinline__ void face_node7(const Slab& sl, const double* __restrict__ fb, const EpiT& epi, int x,
-                                           int y, int z) {
+__device__ __forceinline__ void face_load7(const Slab& sl, const double* __restrict__ fb, const EpiT& epi, int x,
+                                           int y, int z, FaceSite<EpiT>& f) {
   using namespace axw;
   constexpr int q = 7;
-  const int64_t g = sl.lidx(x, y, z);
-  if (sl.masked(x, y, z)) {
-    epi(g, 0.0);
-    return;
-  }
-  constexpr int NC = FAM == 0 ? 8 : (FAM == 1 ? 4 : 2);
-  double v[NC];
+  f.on = true;
+  f.g = sl.lidx(x, y, z);
+  f.masked = sl.masked(x, y, z);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) f.v[c] = 0.0;
   if constexpr (FAM == 0) {
     const Cand2 cx = cand2(x, q, 0, sl.Ex), cy = cand2(y, q, 0, sl.Ey);
     const int ezu = z / q - sl.ez0;  // upper element layer (local k = 0); lower: ezu - 1 (k = q)
@@ -1073,11 +1086,11 @@ __device__ __forceinline__ void face_node7(const Slab& sl, const double* __restr
       for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
         for (int aa = 0; aa < 2; ++aa) {
-          const bool on = zv[c] && (bb ? cy.v1 : cy.v0) && (aa ? cx.v1 : cx.v0);
+          const bool on = !f.masked && zv[c] && (bb ? cy.v1 : cy.v0) && (aa ? cx.v1 : cx.v0);
           const int ey = bb ? cy.e1 : cy.e0, ex = aa ? cx.e1 : cx.e0;
           const int el = ex + sl.Ex * (ey + sl.Ey * (ezu - 1 + c));
           const int fi = (c ? 0 : 64) + (bb ? cy.l1 : cy.l0) * 8 + (aa ? cx.l1 : cx.l0);
-          v[c * 4 + bb * 2 + aa] = on ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
+          f.v[c * 4 + bb * 2 + aa] = on ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
         }
   } else {
     const int ez = z / q, k = z - ez * q;  // interior layer k = 1 .. q-1 of element layer ez
@@ -1090,11 +1103,11 @@ __device__ __forceinline__ void face_node7(const Slab& sl, const double* __restr
       for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
         for (int aa = 0; aa < 2; ++aa) {
-          const bool on = yv[bb] && (aa ? cx.v1 : cx.v0);
+          const bool on = !f.masked && yv[bb] && (aa ? cx.v1 : cx.v0);
           const int ex = aa ? cx.e1 : cx.e0;
           const int el = ex + sl.Ex * (eyu - 1 + bb + sl.Ey * (ez - sl.ez0));
           const int fi = zb + (bb ? 0 : 8) + (aa ? cx.l1 : cx.l0);
-          v[bb * 2 + aa] = on ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
+          f.v[bb * 2 + aa] = on ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
         }
     } else {
       const int ey = y / q, j = y - ey * q;  // interior row j = 1 .. q-1
@@ -1104,14 +1117,26 @@ __device__ __forceinline__ void face_node7(const Slab& sl, const double* __restr
       for (int aa = 0; aa < 2; ++aa) {
         const int el = exu - 1 + aa + sl.Ex * (ey + sl.Ey * (ez - sl.ez0));
         const int fi = zb + 16 + 2 * (j - 1) + (aa ? 0 : 1);
-        v[aa] = xv[aa] ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
+        f.v[aa] = (!f.masked && xv[aa]) ? __ldcs(fb + size_t(el) * FACE + fi) : 0.0;
       }
     }
   }
+  if (!f.masked) f.in = epi.load(f.g);
+}
+
+// Sum in ascending element id (absent contributors and the padding add +0.0: bitwise the sum
+// over the present ones), apply the mask and the epilogue.
+template <class EpiT>
+__device__ __forceinline__ void face_finish7(const FaceSite<EpiT>& f, const EpiT& epi) {
+  if (!f.on) return;
+  if (f.masked) {
+    epi(f.g, 0.0);
+    return;
+  }
   double acc = 0.0;
 #pragma unroll
-  for (int c = 0; c < NC; ++c) acc += v[c];  // ascending element id; absent contributors add +0.0
-  epi(g, acc);
+  for (int c = 0; c < 8; ++c) acc += f.v[c];
+  epi.store(f.g, f.in, acc);
 }
 
 // One launch for the three families: blockIdx.z enumerates the z planes of the slab
@@ -1119,6 +1144,9 @@ __device__ __forceinline__ void face_node7(const Slab& sl, const double* __restr
 //   z % q == 0 (FAM 0): rows y = 0 .. Ny-1, threads over x
 //   z % q != 0: rows 0 .. Ey  are FAM 1 (y = q row, threads over x);
 //               rows Ey+1 .. 2Ey are FAM 2 (y in element row ey = row-Ey-1, threads over (i, y-1-q ey))
+#ifndef SEMLAB_FACE_ROWS
+#define SEMLAB_FACE_ROWS 2  // face rows per block step (loads of all in flight together; 3, 4 slower)
+#endif
 #ifndef SEMLAB_FACE_BLOCKS
 #define SEMLAB_FACE_BLOCKS (148 * 64)  // face-pass blocks (each walks rows with stride gridDim.y)
 #endif
@@ -1130,20 +1158,35 @@ __global__ void __launch_bounds__(128) k_face_epi7(const Slab sl, const double* 
   // rows of each of the 6 nzl planes between them; a block walks rows with stride gridDim.y
   const int ra = (sl.ez1 - sl.ez0 + 1) * sl.Ny, rb = 2 * sl.Ey + 1;
   const int rows = ra + (sl.ez1 - sl.ez0) * (q - 1) * rb;
-  for (int r = int(blockIdx.y); r < rows; r += int(gridDim.y)) {
+  // one face row -> this thread's site in it (f.on = false past the row's end)
+  auto load_row = [&](int r, FaceSite<EpiT>& f) {
+    f.on = false;
     if (r < ra) {
       const int pz = r / sl.Ny, row = r - pz * sl.Ny;
-      if (t < sl.Nx) face_node7<0>(sl, fb, epi, t, row, (sl.ez0 + pz) * q);
-      continue;
+      if (t < sl.Nx) face_load7<0>(sl, fb, epi, t, row, (sl.ez0 + pz) * q, f);
+      return;
     }
     const int rr = r - ra, pl = rr / rb, row = rr - pl * rb;
     const int ez = pl / (q - 1), z = (sl.ez0 + ez) * q + 1 + (pl - ez * (q - 1));
     if (row <= sl.Ey) {
-      if (t < sl.Nx) face_node7<1>(sl, fb, epi, t, row * q, z);
+      if (t < sl.Nx) face_load7<1>(sl, fb, epi, t, row * q, z, f);
     } else {
       const int i = t / (q - 1), yi = t - i * (q - 1);
-      if (i <= sl.Ex) face_node7<2>(sl, fb, epi, i * q, (row - sl.Ey - 1) * q + 1 + yi, z);
+      if (i <= sl.Ex) face_load7<2>(sl, fb, epi, i * q, (row - sl.Ey - 1) * q + 1 + yi, z, f);
     }
+  };
+  // SEMLAB_FACE_ROWS rows per step: all their loads are in flight before any is summed
+  constexpr int NR = SEMLAB_FACE_ROWS;
+  const int gy = int(gridDim.y);
+  for (int r = int(blockIdx.y); r < rows; r += NR * gy) {
+    FaceSite<EpiT> f[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      f[k].on = false;
+      if (r + k * gy < rows) load_row(r + k * gy, f[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < NR; ++k) face_finish7(f[k], epi);
   }
 }
 
