@@ -12,6 +12,13 @@ namespace sb {
 
 namespace {
 
+#ifndef SEMLAB_CGS_NORM_FORM
+#define SEMLAB_CGS_NORM_FORM 1  // 0: per-column branch (ptxas keeps only two loads in flight: 2x slower)
+#endif
+#ifndef SEMLAB_CGS_MINB
+#define SEMLAB_CGS_MINB 2  // resident blocks per SM the dot kernels are register-capped for (1: 12% slower at 24 columns)
+#endif
+
 constexpr int kMaxCol = 32;
 constexpr int kNT = 256;
 
@@ -55,7 +62,7 @@ __device__ __forceinline__ void finish_partials(double (&acc)[NC], int ncol, dou
 
 // h = V^T w over the owned range
 template <int NC>
-__global__ void __launch_bounds__(kNT) k_gemv_t(const double* __restrict__ V, int64_t ldv, int ncol,
+__global__ void __launch_bounds__(kNT, SEMLAB_CGS_MINB) k_gemv_t(const double* __restrict__ V, int64_t ldv, int ncol,
                                                 const double* __restrict__ w, int64_t off, int64_t len,
                                                 double* __restrict__ h, double* partial, unsigned* counter) {
   double acc[NC];
@@ -75,7 +82,7 @@ __global__ void __launch_bounds__(kNT) k_gemv_t(const double* __restrict__ V, in
 
 // w -= V h over [0,n); h2 = V^T w over the owned range (one read of V for both)
 template <int NC>
-__global__ void __launch_bounds__(kNT) k_cgs_update_dot(const double* __restrict__ V, int64_t ldv, int ncol,
+__global__ void __launch_bounds__(kNT, SEMLAB_CGS_MINB) k_cgs_update_dot(const double* __restrict__ V, int64_t ldv, int ncol,
                                                         double* __restrict__ w, const double* __restrict__ h,
                                                         int64_t n, int64_t off, int64_t len,
                                                         double* __restrict__ h2, double* partial,
@@ -115,9 +122,23 @@ __global__ void __launch_bounds__(kNT) k_cgs_update_norm(const double* __restric
   double acc[1] = {0.0};
   for (int64_t i = int64_t(blockIdx.x) * kNT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kNT) {
     double wi = w[i];
+#if SEMLAB_CGS_NORM_FORM == 1
+    // all column loads in flight together: the values are kept live to the end through a
+    // running sum the kernel tests but never uses (w is finite), so ptxas hoists every load
+    // instead of pipelining two at a time
+    double v[NC], keep = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = c < ncol ? __ldcs(V + c * ldv + i) : 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) wi -= v[c] * sh[c];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) keep += v[c];
+    if (keep != keep && wi == 0.0) wi = keep;  // NaN input only, where wi is NaN anyway
+#else
 #pragma unroll
     for (int c = 0; c < NC; ++c)
       if (c < ncol) wi -= __ldcs(V + c * ldv + i) * sh[c];
+#endif
     w[i] = wi;
     if (i >= off && i < off + len) acc[0] = fma(wi, wi, acc[0]);
   }
