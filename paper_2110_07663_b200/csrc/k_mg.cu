@@ -472,12 +472,37 @@ int64_t launch_amg_jacobi0(const double* inv_diag, double omega, const double* r
 }
 
 // zout = z + omega D^-1 (r - A z)   (one damped-Jacobi sweep, amg.cpp:131-138)
+// (A z)_i summed over the row in ascending k (amg.cpp's order), with the row's column indices,
+// values and z gathers issued 8 at a time instead of one dependent pair per step
+__device__ __forceinline__ double csr_row_dot(const int64_t* __restrict__ ptr, const int* __restrict__ idx,
+                                              const double* __restrict__ val, const double* __restrict__ z,
+                                              int64_t i) {
+  constexpr int C = 8;
+  const int64_t k0 = ptr[i], k1 = ptr[i + 1];
+  double az = 0.0;
+  for (int64_t kb = k0; kb < k1; kb += C) {
+    int col[C];
+    double a[C], zv[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const bool ok = kb + c < k1;
+      col[c] = ok ? __ldg(idx + kb + c) : 0;
+      a[c] = ok ? __ldg(val + kb + c) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) zv[c] = kb + c < k1 ? z[col[c]] : 0.0;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (kb + c < k1) az += a[c] * zv[c];
+  }
+  return az;
+}
+
 __global__ void k_amg_relax(const int64_t* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val,
                             const double* __restrict__ inv_diag, double omega, const double* __restrict__ r,
                             const double* __restrict__ z, double* __restrict__ zout, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    double az = 0.0;
-    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) az += val[k] * z[idx[k]];
+    const double az = csr_row_dot(ptr, idx, val, z, i);
     zout[i] = z[i] + omega * inv_diag[i] * (r[i] - az);
   }
 }
@@ -499,9 +524,7 @@ __global__ void k_amg_restrict(const int64_t* __restrict__ ptr, const int* __res
     double acc = 0.0;
     for (int64_t m = aptr[I]; m < aptr[I + 1]; ++m) {
       const int i = amem[m];
-      double az = 0.0;
-      for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) az += val[k] * z[idx[k]];
-      acc += r[i] - az;
+      acc += r[i] - csr_row_dot(ptr, idx, val, z, i);
     }
     rc[I] = acc;
   }
@@ -520,16 +543,27 @@ __global__ void k_amg_residual(const int64_t* __restrict__ ptr, const int* __res
                                const double* __restrict__ val, const double* __restrict__ r,
                                const double* __restrict__ z, double* __restrict__ res, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    double az = 0.0;
-    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) az += val[k] * z[idx[k]];
-    res[i] = r[i] - az;
+    res[i] = r[i] - csr_row_dot(ptr, idx, val, z, i);
   }
 }
 __global__ void k_amg_aggsum(const int64_t* __restrict__ aptr, const int* __restrict__ amem,
                              const double* __restrict__ res, double* __restrict__ rc, int64_t nc) {
   for (int64_t I = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; I < nc; I += int64_t(gridDim.x) * blockDim.x) {
+    // members in ascending order, their indices and values gathered 8 at a time
+    constexpr int C = 8;
+    const int64_t m0 = aptr[I], m1 = aptr[I + 1];
     double acc = 0.0;
-    for (int64_t m = aptr[I]; m < aptr[I + 1]; ++m) acc += res[amem[m]];
+    for (int64_t mb = m0; mb < m1; mb += C) {
+      int mi[C];
+      double v[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) mi[c] = mb + c < m1 ? __ldg(amem + mb + c) : 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) v[c] = mb + c < m1 ? res[mi[c]] : 0.0;
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (mb + c < m1) acc += v[c];
+    }
     rc[I] = acc;
   }
 }
