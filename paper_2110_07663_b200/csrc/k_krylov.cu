@@ -12,9 +12,6 @@ namespace sb {
 
 namespace {
 
-#ifndef SEMLAB_CGS_NORM_FORM
-#define SEMLAB_CGS_NORM_FORM 1  // 0: per-column branch (ptxas keeps only two loads in flight: 2x slower)
-#endif
 #ifndef SEMLAB_CGS_MINB
 #define SEMLAB_CGS_MINB 2  // resident blocks per SM the dot kernels are register-capped for (1: 12% slower at 24 columns)
 #endif
@@ -122,10 +119,9 @@ __global__ void __launch_bounds__(kNT) k_cgs_update_norm(const double* __restric
   double acc[1] = {0.0};
   for (int64_t i = int64_t(blockIdx.x) * kNT + threadIdx.x; i < n; i += int64_t(gridDim.x) * kNT) {
     double wi = w[i];
-#if SEMLAB_CGS_NORM_FORM == 1
     // all column loads in flight together: the values are kept live to the end through a
     // running sum the kernel tests but never uses (w is finite), so ptxas hoists every load
-    // instead of pipelining two at a time
+    // (with a branch per column it kept two in flight and the pass ran at half the rate)
     double v[NC], keep = 0.0;
 #pragma unroll
     for (int c = 0; c < NC; ++c) v[c] = c < ncol ? __ldcs(V + c * ldv + i) : 0.0;
@@ -134,11 +130,6 @@ __global__ void __launch_bounds__(kNT) k_cgs_update_norm(const double* __restric
 #pragma unroll
     for (int c = 0; c < NC; ++c) keep += v[c];
     if (keep != keep && wi == 0.0) wi = keep;  // NaN input only, where wi is NaN anyway
-#else
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < ncol) wi -= __ldcs(V + c * ldv + i) * sh[c];
-#endif
     w[i] = wi;
     if (i >= off && i < off + len) acc[0] = fma(wi, wi, acc[0]);
   }
