@@ -215,7 +215,12 @@ __global__ void __launch_bounds__(EPB* ND* ND, ax_min_blocks<ND>())
     }
     s_grp = t;
   }
-  for (int t = tid; t < ND2; t += NT) s_D[t] = Dm.d[t];
+  // D to shared memory with compile-time indices (a per-thread index into the kernel parameter
+  // would make the compiler copy the whole matrix to a local-memory stack frame in every thread)
+  if (tid == 0) {
+#pragma unroll
+    for (int t = 0; t < ND2; ++t) s_D[t] = Dm.d[t];
+  }
   __syncthreads();
 
   const int64_t nE = sl.elems();
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(ND* ND, axp_minb<ND>())
     k_axp(const Slab sl, const DMat<ND> Dm, const double* __restrict__ u, const GT* __restrict__ geom,
           double* __restrict__ dep, unsigned* __restrict__ flags, unsigned* __restrict__ ticket, int total_tickets,
           const EpiT epi) {
-  constexpr int ND2 = ND * ND, NLOC = ND2 * ND, NT = ND2;
+  constexpr int ND2 = ND * ND, NLOC = ND2 * ND;
   constexpr int q = ND - 1;
   constexpr unsigned GB = unsigned(geom_bytes<GT>(NLOC));
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -458,7 +463,12 @@ __global__ void __launch_bounds__(ND* ND, axp_minb<ND>())
   const int Ex = sl.Ex, Ey = sl.Ey, LZ = Ex * Ey;
   const int Nx = int(sl.Nx), Ny = int(sl.Ny), Nz = int(sl.Nz), NxNy = Nx * Ny;
   const int zlo = int(sl.zlo);
-  for (int t = tid; t < ND2; t += NT) s_D[t] = Dm.d[t];
+  // D to shared memory with compile-time indices (a per-thread index into the kernel parameter
+  // would make the compiler copy the whole matrix to a local-memory stack frame in every thread)
+  if (tid == 0) {
+#pragma unroll
+    for (int t = 0; t < ND2; ++t) s_D[t] = Dm.d[t];
+  }
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     const int t0 = int(atomicAdd(ticket, 1u));
